@@ -1,0 +1,127 @@
+/*
+ * tnsample.h -- C ABI of the B200 boundary-MPS sampler (libtnsample.so).
+ *
+ * Implements the data-parallel hot path of arXiv 2507.11424 (Rudolph & Tindall,
+ * "Simulating and Sampling from Quantum Circuits with 2D Tensor Networks"):
+ * generalised boundary-MPS sampling of bitstrings from a planar tensor-network state.
+ * Citations: P:n = /root/reference/PAPER.md line n; readings R1..R24 = SURVEY.md 8(c),
+ * restated in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Return value: 0 = TN_OK, < 0 = error code below. tn_last_error() returns a
+ *    thread-local, NUL-terminated message for the last failing call on this thread.
+ *  - Host pointers are borrowed for the duration of the call only (copied to the device).
+ *    "_dev" variants take device pointers and a cudaStream_t (passed as void*), do not
+ *    synchronise the stream, and leave the caller responsible for the buffers' lifetime
+ *    until the stream has passed the call.
+ *  - A tn_state is owned by the caller from tn_load_state until tn_free_state. Calls on one
+ *    state must be serialised by the caller; distinct states may be used concurrently.
+ *    The state is immutable after load except for internal caches keyed by
+ *    (row order, chi_env): the device layout of the tensors and the norm environments.
+ *  - All work runs on the CUDA device current at tn_load_state. There is no CPU fallback:
+ *    without a usable device, calls fail with TN_E_CUDA.
+ */
+#ifndef TNSAMPLE_H
+#define TNSAMPLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TN_OK 0
+#define TN_E_ARG (-1)     /* NULL pointer, n <= 0, chi_env < 1, uniform not finite or not in [0,1) */
+#define TN_E_GRAPH (-2)   /* vertex id out of range, self-loop, duplicate edge, bond dim not in [1,chi],
+                             tensor shape inconsistent with the graph */
+#define TN_E_ROWS (-3)    /* row order not a grid-layered line partition (R1) */
+#define TN_E_NOMEM (-4)   /* device or host allocation failed */
+#define TN_E_CUDA (-5)    /* CUDA runtime error or no device */
+#define TN_E_NCCL (-6)    /* reserved: collectives run in the Python driver (torch.distributed) */
+#define TN_E_NUMERIC (-7) /* non-finite value in the norm-environment precompute */
+
+/* Per-sample incident flags (not errors). */
+#define TN_FLAG_CLAMPED 1u   /* a one-site weight Re w_s < 0 was clamped to 0 */
+#define TN_FLAG_ZERO_MASS 2u /* w_0 + w_1 == 0: P0 := 1/2 was used */
+#define TN_FLAG_NONFINITE 4u /* a non-finite weight appeared; logp is NaN */
+
+typedef struct tn_state tn_state; /* opaque */
+
+/* Graph of the tensor network state |psi> (one tensor per qubit, one virtual
+ * index per edge). edges: [n_edges][2] vertex ids, 0 <= u,v < n_vertices, u != v, no
+ * duplicates. bond_dims: [n_edges], 1 <= dim <= chi. */
+typedef struct {
+  int32_t n_vertices;
+  int32_t n_edges;
+  const int32_t* edges;
+  const int32_t* bond_dims;
+} tn_graph;
+
+/* Load a TNS (D1). tensors[v] points to interleaved complex128 (re, im) data in
+ * C order with shape (2, d_e1, d_e2, ...), where e1 < e2 < ... are the ids of the edges
+ * incident to v (physical index first). chi >= max bond dim. The data are converted to
+ * complex64 on the device (R24). On success *out owns a new state. */
+int tn_load_state(const tn_graph* g, const double* const* tensors, int32_t chi, tn_state** out);
+
+/* Norm-environment precompute (a1, "contract the norm network once (independent of the
+ * number of samples)"): M_{N_b -> N_b-1} ... M_{2->1} at bond <= chi_env for the row
+ * order given as CSR: row_ptr[n_rows+1], row_vertices[n_vertices] (the partition b = 1..N_b
+ * in sampling order, vertices of a row in their within-row order, R1/R2). Cached in the
+ * state; tn_sample calls it implicitly when the cache misses. Sets the state's current
+ * row order (used by tn_amplitude). */
+int tn_prepare(tn_state* st, const int32_t* row_ptr, const int32_t* row_vertices, int32_t n_rows,
+               int32_t chi_env);
+
+/* Draw n_samples bitstrings from q(x). uniforms[k][v] in [0,1) is
+ * the random number of sample k at vertex id v: x_v = 0 iff u < P0 (R10). Outputs are
+ * caller-allocated host arrays: out_bits[k][v] in {0,1} by vertex id, out_logp[k] =
+ * ln q(x_k), the natural log of the product of the sampled conditionals (R11). */
+int tn_sample(tn_state* st, const int32_t* row_ptr, const int32_t* row_vertices, int32_t n_rows,
+              int32_t chi_env, int64_t n_samples, const double* uniforms, uint8_t* out_bits,
+              double* out_logp);
+
+/* Extended form. sample_offset: global index of the first sample (bookkeeping only; the
+ * uniforms given are used as-is, so results do not depend on batching or GPU count,
+ * SURVEY 8(b) "Determinism"). out_cond[k][v] (optional, may be NULL): P(x_v | earlier
+ * vertices) of the drawn bit. out_flags[k] (optional): OR of TN_FLAG_*. */
+int tn_sample_ex(tn_state* st, const int32_t* row_ptr, const int32_t* row_vertices, int32_t n_rows,
+                 int32_t chi_env, int64_t n_samples, int64_t sample_offset, const double* uniforms,
+                 uint8_t* out_bits, double* out_logp, double* out_cond, uint32_t* out_flags);
+
+/* Device-pointer form of tn_sample_ex (for the torch driver / benchmarks): uniforms_dev
+ * [n][N] float64, out_bits_dev [n][N] uint8, out_logp_dev [n] float64, out_cond_dev and
+ * out_flags_dev optional (NULL). stream: cudaStream_t or NULL for the legacy stream.
+ * Requires a prior tn_prepare for this row order and chi_env (TN_E_ROWS otherwise). */
+int tn_sample_dev(tn_state* st, const int32_t* row_ptr, const int32_t* row_vertices, int32_t n_rows,
+                  int32_t chi_env, int64_t n_samples, const double* uniforms_dev, uint8_t* out_bits_dev,
+                  double* out_logp_dev, double* out_cond_dev, uint32_t* out_flags_dev, void* stream);
+
+/* Amplitudes <x|psi> (D3) of n bitstrings bits[k][v] (by vertex id), contracted by
+ * boundary MPS of bond <= chi_env over the state's current row order (the last one given to
+ * tn_prepare / tn_sample; TN_E_ROWS if none) ("separate contraction of
+ * the network <x|psi>"). out_logabs[k] = ln|<x|psi>| (-inf for an exactly zero amplitude),
+ * out_phase[k] = arg <x|psi> in radians. Unnormalised: sum_x |<x|psi>|^2 = <psi|psi>. */
+int tn_amplitude(tn_state* st, const uint8_t* bits, int64_t n, int32_t chi_env, double* out_logabs,
+                 double* out_phase);
+
+/* ln <psi|psi> ~ ln <M_{2->1}, T_1> for the current row order and chi_env (R12). */
+int tn_log_norm(tn_state* st, int32_t chi_env, double* out_lognorm);
+
+/* Options (SURVEY 5 "Config / flags"): "fit_half_sweeps" (nh, default 2, R5), "init_seed"
+ * (default 0x2507114240, R4), "gemm" (0 = auto, 1 = force SIMT FP32, 2 = force tcgen05
+ * TF32x3), "max_batch" (0 = auto from free device memory). Changing an option invalidates
+ * cached environments. Unknown name -> TN_E_ARG. */
+int tn_set_option(tn_state* st, const char* name, int64_t value);
+
+/* Kernel launches and wall-clock of the last call on this state (instrumentation). */
+int tn_get_stats(tn_state* st, int64_t* out_launches, double* out_precompute_s);
+
+int tn_free_state(tn_state* st);
+
+const char* tn_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TNSAMPLE_H */

@@ -1,0 +1,9 @@
+"""paper_2507_11424_b200 -- B200-native boundary-MPS bitstring sampling (arXiv 2507.11424).
+
+The product path is libtnsample.so (CUDA, sm_100a) behind the C ABI of include/tnsample.h;
+this package is the thin ctypes binding (argument marshalling only) plus the multi-GPU
+driver helpers. There is no CPU fallback.
+"""
+from ._lib import TNError, TNState, lib, load_library  # noqa: F401
+
+__all__ = ["TNState", "TNError", "lib", "load_library"]

@@ -1,0 +1,318 @@
+// fit.cu -- one-site MPS-MPO fitting on the device (see fit.h).
+//
+// Follows O3 step by step (restated in DESIGN.md): hash init (R4), right-
+// orthonormalisation as a true gauge transformation, right environments, nh alternating
+// half-sweeps replacing each site by the derivative of <o|T> and
+// re-orthonormalising it (exact D_k columns, R6/R7), the turning site not recomputed,
+// final centre normalised.
+#include <algorithm>
+
+#include "fit.h"
+#include "kernels.h"
+#include "linalg.h"
+
+namespace tn {
+namespace {
+
+Tensor view(const Tensor& t, std::vector<int> shape) {
+  Tensor v = t;
+  v.shape = std::move(shape);
+  return v;
+}
+
+Tensor slice_rows(const Tensor& t, int x0, int x1) {
+  Tensor v = t;
+  int64_t row = t.size() / t.shape[0];
+  v.p = t.p + x0 * row;
+  v.shape[0] = x1 - x0;
+  return v;
+}
+
+int row_bond(const DStrip& s, int j) { return s.dbl ? s.mats[j].shape[3] : s.mats[j].shape[2]; }
+
+int p_dim(const DStrip& s, int j) {
+  if (s.dbl) return s.mats[j].shape[1] * s.mats[j].shape[1];
+  return s.mats[j].shape[1];
+}
+
+std::vector<int> o_shape(const DStrip& s, int j, int dl, int dr) {
+  if (s.dbl) return {dl, s.mats[j].shape[1], s.mats[j].shape[1], dr};
+  return {dl, s.mats[j].shape[1], dr};
+}
+
+struct Ops {
+  Ctx& c;
+  const DStrip& s;
+  int nb() const { return s.per_sample ? c.nb : 1; }
+  Tensor trivial() {
+    Tensor t = ones(c, s.dbl ? std::vector<int>{1, 1, 1, 1} : std::vector<int>{1, 1, 1}, nb());
+    if (!s.per_sample) t.bstride = 0;  // shared: every derived tensor stays shared
+    return t;
+  }
+
+  // ---------------- single layer
+  Tensor mid1(const Tensor& L, int j) {
+    const Tensor& B = s.mats[j];
+    if (s.tops[j].p) {
+      Tensor X1 = contract(c, L, "xmy", false, s.tops[j], "mun", false, "xyun");
+      return contract(c, X1, "xyun", false, B, "upyr", false, "xnpr");
+    }
+    return contract(c, L, "xny", false, B, "upyr", false, "xnpr");
+  }
+
+  // ---------------- double layer, rows [x0,x1) of the output-bond index
+  Tensor mid2(const Tensor& L, int j, int x0, int x1) {
+    const Tensor& A = s.mats[j];
+    Tensor Lc = slice_rows(L, x0, x1);
+    Tensor X2;
+    if (s.tops[j].p) {
+      Tensor X1 = contract(c, Lc, "xeab", false, s.tops[j], "edDf", false, "xabdDf");
+      X2 = contract(c, X1, "xabdDf", false, A, "sudar", false, "xbDfsur");
+    } else {
+      X2 = contract(c, Lc, "xfab", false, A, "sudar", false, "xbDfsur");
+    }
+    return contract(c, X2, "xbDfsur", false, A, "sUDbR", true, "xfurUR");
+  }
+
+  int chunk_rows(int j, int nx) {
+    const Tensor& A = s.mats[j];
+    int64_t u = A.shape[1], d = A.shape[2], l = A.shape[3], r = A.shape[4];
+    int64_t f = s.tops[j].p ? s.tops[j].shape[3] : s.topbond[j];
+    int64_t per = std::max({l * l * d * d * f, 2 * l * d * f * u * r, f * u * u * r * r, f * r * r * u * u});
+    int64_t rows = std::max<int64_t>(1, s.chunk_elems / std::max<int64_t>(1, per));
+    return (int)std::min<int64_t>(rows, nx);
+  }
+
+  Tensor absorb_left(const Tensor& L, int j, const Tensor* o) {
+    if (!s.dbl) {
+      Tensor X = mid1(L, j);
+      if (!o) return view(X, {X.shape[0], X.shape[1], X.shape[3]});
+      return contract(c, X, "xnpr", false, *o, "xpz", true, "znr");
+    }
+    int nx = L.shape[0];
+    int step = chunk_rows(j, nx);
+    Tensor out;
+    for (int x0 = 0; x0 < nx; x0 += step) {
+      int x1 = std::min(nx, x0 + step);
+      Tensor X = mid2(L, j, x0, x1);
+      if (!o) {
+        Tensor part = view(X, {X.shape[0], X.shape[1], X.shape[3], X.shape[5]});
+        if (step >= nx) return part;
+        if (!out.p) out = new_tensor(c, {nx, part.shape[1], part.shape[2], part.shape[3]}, false);
+        copy_rows(c, part, out, x0, 1);
+      } else {
+        Tensor oc = slice_rows(*o, x0, x1);
+        Tensor part = contract(c, X, "xfurUR", false, oc, "xuUz", true, "zfrR");
+        if (!out.p) out = part;
+        else add_into(c, out, part, 1);
+      }
+    }
+    return out;
+  }
+
+  Tensor derivative(const Tensor& L, int j, const Tensor& F) {
+    if (!s.dbl) {
+      Tensor X = mid1(L, j);
+      return contract(c, X, "xnpr", false, F, "znr", false, "xpz");
+    }
+    int nx = L.shape[0];
+    int step = chunk_rows(j, nx);
+    Tensor out;
+    for (int x0 = 0; x0 < nx; x0 += step) {
+      int x1 = std::min(nx, x0 + step);
+      Tensor X = mid2(L, j, x0, x1);
+      Tensor part = contract(c, X, "xfurUR", false, F, "zfrR", false, "xuUz");
+      if (step >= nx) return part;
+      if (!out.p) out = new_tensor(c, {nx, part.shape[1], part.shape[2], part.shape[3]}, false);
+      copy_rows(c, part, out, x0, 1);
+    }
+    return out;
+  }
+
+  Tensor absorb_right(const Tensor& F, int j, const Tensor* o) {
+    if (!s.dbl) {
+      const Tensor& B = s.mats[j];
+      Tensor Y2;
+      if (o) {
+        Tensor Y1 = contract(c, F, "znr", false, *o, "xpz", true, "nrxp");
+        Y2 = contract(c, Y1, "nrxp", false, B, "upyr", false, "nxuy");
+      } else {
+        Y2 = contract(c, F, "xnr", false, B, "upyr", false, "nxuy");
+      }
+      if (s.tops[j].p) return contract(c, Y2, "nxuy", false, s.tops[j], "mun", false, "xmy");
+      Tensor Y2v = view(Y2, {Y2.shape[0], Y2.shape[1], Y2.shape[3]});
+      return permute(c, Y2v, "nxy", "xny");
+    }
+    const Tensor& A = s.mats[j];
+    int nx = o ? o->shape[0] : F.shape[0];
+    int step = chunk_rows(j, nx);
+    Tensor out;
+    for (int x0 = 0; x0 < nx; x0 += step) {
+      int x1 = std::min(nx, x0 + step);
+      Tensor Y2;
+      if (o) {
+        Tensor oc = slice_rows(*o, x0, x1);
+        Tensor Y1 = contract(c, F, "zfrR", false, oc, "xuUz", true, "frRxuU");
+        Y2 = contract(c, Y1, "frRxuU", false, A, "sudar", false, "fRxUsda");
+      } else {
+        Tensor Fc = slice_rows(F, x0, x1);  // non-output column: u = U = 1
+        Y2 = contract(c, Fc, "xfrR", false, A, "sudar", false, "fRxUsda");
+      }
+      Tensor Y3 = contract(c, Y2, "fRxUsda", false, A, "sUDbR", true, "fxdaDb");
+      Tensor part;
+      if (s.tops[j].p) {
+        part = contract(c, Y3, "fxdaDb", false, s.tops[j], "edDf", false, "xeab");
+      } else {
+        Tensor Y3v = view(Y3, {Y3.shape[0], Y3.shape[1], Y3.shape[3], Y3.shape[5]});
+        part = permute(c, Y3v, "fxab", "xfab");
+      }
+      if (step >= nx) return part;
+      if (!out.p) out = new_tensor(c, {nx, part.shape[1], part.shape[2], part.shape[3]}, false);
+      copy_rows(c, part, out, x0, 1);
+    }
+    return out;
+  }
+};
+
+// column span of o reshaped (prod(shape[:-1])) x shape[-1]
+Tensor left_orth(Ctx& c, const Tensor& o, int nb) {
+  Tensor q = new_tensor_n(c, o.shape, nb);
+  if (!o.bstride) q.bstride = 0;
+  int n = o.shape.back();
+  int m = (int)(o.size() / n);
+  MatView X{o.p, o.bstride, n, 1, false, m, n};
+  MatView Q{q.p, q.bstride, n, 1, false, m, n};
+  orthonormalize(c, X, Q, nullptr, o.bstride ? nb : 1);
+  return q;
+}
+
+// row span of o reshaped shape[0] x (rest); optional C with o = C^H-factor (see linalg.h)
+Tensor right_orth(Ctx& c, const Tensor& o, int nb, Tensor* Cout) {
+  Tensor q = new_tensor_n(c, o.shape, nb);
+  if (!o.bstride) q.bstride = 0;
+  int dl = o.shape[0];
+  int rest = (int)(o.size() / dl);
+  MatView X{o.p, o.bstride, 1, rest, true, rest, dl};
+  MatView Q{q.p, q.bstride, 1, rest, true, rest, dl};
+  float2* cp = nullptr;
+  if (Cout) {
+    *Cout = new_tensor_n(c, {dl, dl}, nb);
+    if (!o.bstride) Cout->bstride = 0;
+    cp = Cout->p;
+  }
+  orthonormalize(c, X, Q, cp, o.bstride ? nb : 1);
+  return q;
+}
+
+}  // namespace
+
+std::vector<int> fit_bonds(const DStrip& s, int R) {
+  std::vector<int> cols;
+  for (int j = 0; j < s.W; ++j)
+    if (s.out[j]) cols.push_back(j);
+  int K = (int)cols.size();
+  std::vector<int64_t> D(K + 1, 1);
+  for (int k = 1; k < K; ++k) {
+    int64_t cut = INT64_MAX;
+    for (int j = cols[k - 1] + 1; j <= cols[k]; ++j) {
+      int64_t r = row_bond(s, j);
+      int64_t cd = (int64_t)s.topbond[j] * (s.dbl ? r * r : r);
+      cut = std::min(cut, cd);
+    }
+    D[k] = std::min<int64_t>(R, cut);
+  }
+  std::vector<int64_t> p(K);
+  for (int k = 0; k < K; ++k) p[k] = p_dim(s, cols[k]);
+  for (int k = 1; k < K; ++k) D[k] = std::min(D[k], D[k - 1] * p[k - 1]);
+  for (int k = K - 1; k >= 1; --k) D[k] = std::min(D[k], p[k] * D[k + 1]);
+  return std::vector<int>(D.begin(), D.end());
+}
+
+FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, int nh, double* logn,
+              bool accumulate) {
+  Ops ops{c, s};
+  int nb = ops.nb();
+  FitResult res;
+  std::vector<int> cols;
+  for (int j = 0; j < s.W; ++j)
+    if (s.out[j]) cols.push_back(j);
+  int K = (int)cols.size();
+  if (K == 0) {
+    Tensor L = ops.trivial();
+    for (int j = 0; j < s.W; ++j) L = ops.absorb_left(L, j, nullptr);
+    res.scalar = L;
+    return res;
+  }
+  std::vector<int> D = fit_bonds(s, R);
+  std::vector<Tensor> o(K);
+  for (int k = 0; k < K; ++k) {
+    o[k] = new_tensor_n(c, o_shape(s, cols[k], D[k], D[k + 1]), nb);
+    if (!s.per_sample) o[k].bstride = 0;
+    hash_init(c, o[k], nb, seed, tag, b1, k);
+  }
+  // right-orthonormalise as a true gauge transformation (absorb the factor to the left)
+  for (int k = K - 1; k >= 1; --k) {
+    Tensor C;
+    Tensor q = right_orth(c, o[k], nb, &C);
+    o[k] = q;
+    // o_{k-1}[..., b] <- sum_q o_{k-1}[..., q] conj(C[b, q])
+    const Tensor& prev = o[k - 1];
+    std::vector<int> sh2 = {(int)(prev.size() / prev.shape.back()), prev.shape.back()};
+    Tensor pv = view(prev, sh2);
+    Tensor np = contract(c, pv, "aq", false, C, "bq", true, "ab");
+    o[k - 1] = view(np, prev.shape);
+  }
+  auto env_left = [&](const Tensor& Lk, int k) {
+    Tensor L = ops.absorb_left(Lk, cols[k], &o[k]);
+    int end = (k + 1 < K) ? cols[k + 1] : s.W;
+    for (int j = cols[k] + 1; j < end; ++j) L = ops.absorb_left(L, j, nullptr);
+    return L;
+  };
+  auto env_right = [&](const Tensor& Fk, int k) {
+    Tensor F = ops.absorb_right(Fk, cols[k], &o[k]);
+    int start = (k >= 1) ? cols[k - 1] : -1;
+    for (int j = cols[k] - 1; j > start; --j) F = ops.absorb_right(F, j, nullptr);
+    return F;
+  };
+  std::vector<Tensor> Lk(K), Fk(K);
+  {
+    Tensor L = ops.trivial();
+    for (int j = 0; j < cols[0]; ++j) L = ops.absorb_left(L, j, nullptr);
+    Lk[0] = L;
+    Tensor F = ops.trivial();
+    for (int j = s.W - 1; j > cols[K - 1]; --j) F = ops.absorb_right(F, j, nullptr);
+    Fk[K - 1] = F;
+  }
+  for (int k = K - 1; k >= 1; --k) Fk[k - 1] = env_right(Fk[k], k);
+  for (int h = 0; h < nh; ++h) {
+    if (h % 2 == 0) {
+      for (int k = 0; k < K; ++k) {
+        if (!(h > 0 && k == 0)) {
+          Tensor d = ops.derivative(Lk[k], cols[k], Fk[k]);
+          o[k] = view(d, o[k].shape);
+        }
+        if (k < K - 1) {
+          o[k] = left_orth(c, o[k], nb);
+          Lk[k + 1] = env_left(Lk[k], k);
+        }
+      }
+    } else {
+      for (int k = K - 1; k >= 0; --k) {
+        if (k != K - 1) {
+          Tensor d = ops.derivative(Lk[k], cols[k], Fk[k]);
+          o[k] = view(d, o[k].shape);
+        }
+        if (k > 0) {
+          o[k] = right_orth(c, o[k], nb, nullptr);
+          Fk[k - 1] = env_right(Fk[k], k);
+        }
+      }
+    }
+  }
+  int centre = (nh % 2 == 1) ? K - 1 : 0;
+  normalize(c, o[centre], nb, logn, accumulate);
+  res.sites = std::move(o);
+  return res;
+}
+
+}  // namespace tn

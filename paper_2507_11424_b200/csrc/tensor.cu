@@ -1,0 +1,482 @@
+// tensor.cu -- device tensors, permutation kernel, FP32 SIMT complex GEMM and the
+// contraction planner (see tensor.h).
+#include <algorithm>
+#include <cstring>
+#include <map>
+
+#include "tensor.h"
+
+namespace tn {
+
+int64_t g_launches = 0;
+double g_cmacs = 0.0;
+
+// tcgen05 path (gemm_tc.cu); returns false when the shape/layout is not eligible.
+bool gemm_tc(Ctx& c, const GemmDesc& g);
+
+Tensor new_tensor_n(Ctx& c, const std::vector<int>& shape, int nb) {
+  Tensor t;
+  t.shape = shape;
+  int64_t sz = prod(shape);
+  t.bstride = nb > 1 ? sz : (nb == 1 ? sz : 0);
+  size_t bytes = (size_t)std::max<int64_t>(1, sz * std::max(nb, 1)) * sizeof(float2);
+  t.mem = std::make_shared<DevBuf>(bytes, c.stream);
+  t.p = t.mem->as<float2>();
+  return t;
+}
+
+Tensor new_tensor(Ctx& c, const std::vector<int>& shape, bool per_sample) {
+  Tensor t = new_tensor_n(c, shape, per_sample ? c.nb : 1);
+  if (!per_sample) t.bstride = 0;
+  return t;
+}
+
+void zero(Ctx& c, Tensor& t, int nb) {
+  int64_t n = t.bstride ? t.bstride * nb : t.size();
+  TN_CUDA(cudaMemsetAsync(t.p, 0, (size_t)n * sizeof(float2), c.stream));
+}
+
+// ----------------------------------------------------------------------------- permute
+struct PermArgs {
+  int rank;
+  int64_t dims[8];      // output dims
+  int64_t istride[8];   // input stride of each output axis
+  int64_t size;         // elements per sample
+  int64_t ibs, obs;     // sample strides
+  int nb;
+  bool conj;
+};
+
+__global__ void permute_kernel(const float2* __restrict__ in, float2* __restrict__ out, PermArgs a) {
+  int64_t total = a.size * a.nb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = i / a.size, r = i - b * a.size;
+    int64_t off = 0, rem = r;
+#pragma unroll
+    for (int d = 7; d >= 0; --d) {
+      if (d < a.rank) {
+        int64_t q = rem / a.dims[d];
+        int64_t idx = rem - q * a.dims[d];
+        off += idx * a.istride[d];
+        rem = q;
+      }
+    }
+    float2 v = in[b * a.ibs + off];
+    if (a.conj) v.y = -v.y;
+    out[b * a.obs + r] = v;
+  }
+}
+
+// 2D tiled transpose for the common case "swap two compound groups" is left for later; the
+// generic kernel above is L2-assisted and HBM-bound on the large ladder intermediates.
+
+static std::vector<int64_t> strides_of(const std::vector<int>& shape) {
+  std::vector<int64_t> s(shape.size());
+  int64_t acc = 1;
+  for (int i = (int)shape.size() - 1; i >= 0; --i) {
+    s[i] = acc;
+    acc *= shape[i];
+  }
+  return s;
+}
+
+Tensor permute(Ctx& c, const Tensor& A, const char* la, const char* lout, bool conj) {
+  int r = (int)strlen(la);
+  if (r != A.rank() || (int)strlen(lout) != r) throw Error(-1, "permute: label/rank mismatch");
+  auto st = strides_of(A.shape);
+  std::vector<int> oshape(r);
+  PermArgs a{};
+  a.rank = 0;
+  // drop unit dims, merge nothing (simple)
+  std::vector<int64_t> dims, istr;
+  for (int i = 0; i < r; ++i) {
+    const char* q = strchr(la, lout[i]);
+    if (!q) throw Error(-1, "permute: unknown label");
+    int j = (int)(q - la);
+    oshape[i] = A.shape[j];
+    if (A.shape[j] != 1) {
+      dims.push_back(A.shape[j]);
+      istr.push_back(st[j]);
+    }
+  }
+  if (dims.size() > 8) throw Error(-1, "permute: rank > 8");
+  int nb = A.bstride ? c.nb : 1;
+  Tensor out = new_tensor_n(c, oshape, nb);
+  if (!A.bstride) out.bstride = 0;
+  a.rank = (int)dims.size();
+  for (int i = 0; i < a.rank; ++i) {
+    a.dims[i] = dims[i];
+    a.istride[i] = istr[i];
+  }
+  a.size = A.size();
+  a.ibs = A.bstride;
+  a.obs = out.bstride;
+  a.nb = nb;
+  a.conj = conj;
+  int64_t total = a.size * nb;
+  if (total == 0) return out;
+  unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  permute_kernel<<<blocks, 256, 0, c.stream>>>(A.p, out.p, a);
+  TN_LAUNCHED();
+  return out;
+}
+
+// ----------------------------------------------------------------------------- SIMT GEMM
+// 64x64 complex tile, BK = 8, 256 threads, 4x4 complex outputs per thread, FP32 FMA.
+// Used for shapes the tcgen05 kernel does not take (small or unaligned) and as the
+// forced path gemm=1.
+namespace {
+constexpr int BM = 64, BN = 64, BK = 8, PAD = 2;
+
+__device__ __forceinline__ float2 ld_c(const float2* p, bool cj) {
+  float2 v = __ldg(p);
+  if (cj) v.y = -v.y;
+  return v;
+}
+
+__global__ void __launch_bounds__(256) cgemm_simt(GemmDesc g) {
+  __shared__ __align__(16) float2 As[BK][BM + PAD];
+  __shared__ __align__(16) float2 Bs[BK][BN + PAD];
+  int bz = blockIdx.z;
+  int b1 = bz / g.nb2, b2 = bz - b1 * g.nb2;
+  const float2* A = g.A + b1 * g.sa1 + b2 * g.sa2;
+  const float2* B = g.B + b1 * g.sb1 + b2 * g.sb2;
+  float2* C = g.C + b1 * g.sc1 + b2 * g.sc2;
+  int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  int t = threadIdx.x;
+  int tx = t & 15, ty = t >> 4;
+  float2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  const bool a_kc = (g.ak == 1);
+  const bool b_nc = (g.bn == 1);
+  float2 ra[2], rb[2];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      int e = t + 256 * i;
+      int m, k;
+      if (a_kc) { m = e >> 3; k = e & 7; } else { m = e & 63; k = e >> 6; }
+      int gm = m0 + m, gk = k0 + k;
+      ra[i] = (gm < g.M && gk < g.K) ? ld_c(A + gm * g.am + gk * g.ak, g.conjA) : make_float2(0.f, 0.f);
+      int n;
+      if (b_nc) { n = e & 63; k = e >> 6; } else { n = e >> 3; k = e & 7; }
+      int gn = n0 + n;
+      gk = k0 + k;
+      rb[i] = (gn < g.N && gk < g.K) ? ld_c(B + gk * g.bk + gn * g.bn, g.conjB) : make_float2(0.f, 0.f);
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      int e = t + 256 * i;
+      int m, k;
+      if (a_kc) { m = e >> 3; k = e & 7; } else { m = e & 63; k = e >> 6; }
+      As[k][m] = ra[i];
+      int n;
+      if (b_nc) { n = e & 63; k = e >> 6; } else { n = e >> 3; k = e & 7; }
+      Bs[k][n] = rb[i];
+    }
+  };
+  load(0);
+  for (int k0 = 0; k0 < g.K; k0 += BK) {
+    store();
+    __syncthreads();
+    if (k0 + BK < g.K) load(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float4 a01 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      float4 a23 = *reinterpret_cast<const float4*>(&As[kk][ty * 4 + 2]);
+      float4 b01 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      float4 b23 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4 + 2]);
+      float2 a[4] = {{a01.x, a01.y}, {a01.z, a01.w}, {a23.x, a23.y}, {a23.z, a23.w}};
+      float2 b[4] = {{b01.x, b01.y}, {b01.z, b01.w}, {b23.x, b23.y}, {b23.z, b23.w}};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[i][j].x = fmaf(a[i].x, b[j].x, acc[i][j].x);
+          acc[i][j].x = fmaf(-a[i].y, b[j].y, acc[i][j].x);
+          acc[i][j].y = fmaf(a[i].x, b[j].y, acc[i][j].y);
+          acc[i][j].y = fmaf(a[i].y, b[j].x, acc[i][j].y);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int gm = m0 + ty * 4 + i;
+    if (gm >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gn = n0 + tx * 4 + j;
+      if (gn >= g.N) continue;
+      float2* cp = C + (int64_t)gm * g.cm + gn;
+      if (g.accumulate) {
+        float2 o = *cp;
+        o.x += acc[i][j].x;
+        o.y += acc[i][j].y;
+        *cp = o;
+      } else {
+        *cp = acc[i][j];
+      }
+    }
+  }
+}
+}  // namespace
+
+void gemm(Ctx& c, const GemmDesc& g) {
+  if (g.M <= 0 || g.N <= 0 || g.nb1 <= 0 || g.nb2 <= 0) return;
+  g_cmacs += (double)g.M * g.N * std::max(g.K, 0) * g.nb1 * g.nb2;
+  if (g.K <= 0) {
+    if (!g.accumulate) {
+      // C = 0 (empty contraction): handled by the planner allocating zeroed outputs
+    }
+    return;
+  }
+  if (c.gemm_mode != 1 && gemm_tc(c, g)) return;
+  int64_t nbz = (int64_t)g.nb1 * g.nb2;
+  if (nbz > 65535) {
+    // split the outer batch into chunks
+    GemmDesc h = g;
+    int per = std::max(1, 65535 / g.nb2);
+    for (int b0 = 0; b0 < g.nb1; b0 += per) {
+      h.nb1 = std::min(per, g.nb1 - b0);
+      h.A = g.A + b0 * g.sa1;
+      h.B = g.B + b0 * g.sb1;
+      h.C = g.C + b0 * g.sc1;
+      gemm(c, h);
+    }
+    g_cmacs -= (double)g.M * g.N * g.K * g.nb1 * g.nb2;
+    return;
+  }
+  dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, BM), (unsigned)nbz);
+  if (grid.y > 65535) {
+    GemmDesc h = g;
+    int rows = 65535 * BM;
+    for (int m0 = 0; m0 < g.M; m0 += rows) {
+      h.M = std::min(rows, g.M - m0);
+      h.A = g.A + (int64_t)m0 * g.am;
+      h.C = g.C + (int64_t)m0 * g.cm;
+      gemm(c, h);
+      g_cmacs -= (double)h.M * h.N * h.K * h.nb1 * h.nb2;
+    }
+    return;
+  }
+  cgemm_simt<<<grid, 256, 0, c.stream>>>(g);
+  TN_LAUNCHED();
+}
+
+// ----------------------------------------------------------------------------- planner
+namespace {
+struct Op {
+  const Tensor* t;
+  std::string lab;          // labels without unit dims
+  std::vector<int> dims;    // matching dims
+  std::vector<int64_t> str; // matching strides
+  bool conj;
+};
+
+Op make_op(const Tensor& t, const char* l, bool cj) {
+  Op o{&t, "", {}, {}, cj};
+  int r = (int)strlen(l);
+  if (r != t.rank()) throw Error(-1, std::string("contract: rank mismatch for labels ") + l);
+  auto st = strides_of(t.shape);
+  for (int i = 0; i < r; ++i)
+    if (t.shape[i] != 1) {
+      o.lab.push_back(l[i]);
+      o.dims.push_back(t.shape[i]);
+      o.str.push_back(st[i]);
+    }
+  return o;
+}
+
+// If the labels `grp` (in this order) occupy consecutive axes of op, return the stride of
+// the compound index (stride of the last one); -1 otherwise. Empty group -> 0.
+int64_t group_stride(const Op& o, const std::string& grp) {
+  if (grp.empty()) return 0;
+  size_t p0 = o.lab.find(grp[0]);
+  if (p0 == std::string::npos) return -1;
+  for (size_t i = 0; i < grp.size(); ++i)
+    if (p0 + i >= o.lab.size() || o.lab[p0 + i] != grp[i]) return -1;
+  return o.str[p0 + grp.size() - 1];
+}
+
+std::string order_in(const std::string& lab, const std::string& set) {
+  std::string r;
+  for (char ch : lab)
+    if (set.find(ch) != std::string::npos) r.push_back(ch);
+  return r;
+}
+}  // namespace
+
+Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Tensor& B0,
+                const char* lb0, bool conjB0, const char* lout) {
+  // dims of every label
+  std::map<char, int> dim;
+  auto reg = [&](const Tensor& t, const char* l) {
+    int r = (int)strlen(l);
+    if (r != t.rank()) throw Error(-1, std::string("contract: rank mismatch ") + l);
+    for (int i = 0; i < r; ++i) {
+      auto it = dim.find(l[i]);
+      if (it != dim.end() && it->second != t.shape[i])
+        throw Error(-1, std::string("contract: dim mismatch on label ") + l[i]);
+      dim[l[i]] = t.shape[i];
+    }
+  };
+  reg(A0, la0);
+  reg(B0, lb0);
+  std::vector<int> oshape;
+  for (const char* q = lout; *q; ++q) {
+    auto it = dim.find(*q);
+    if (it == dim.end()) {  // a label absent from both operands is a unit axis
+      dim[*q] = 1;
+      oshape.push_back(1);
+    } else {
+      oshape.push_back(it->second);
+    }
+  }
+  // left operand = the per-sample one when the other is shared
+  bool swap = (A0.bstride == 0 && B0.bstride != 0);
+  const Tensor& X = swap ? B0 : A0;
+  const Tensor& Y = swap ? A0 : B0;
+  const char* lx = swap ? lb0 : la0;
+  const char* ly = swap ? la0 : lb0;
+  bool cx = swap ? conjB0 : conjA0, cy = swap ? conjA0 : conjB0;
+  Op ox = make_op(X, lx, cx), oy = make_op(Y, ly, cy);
+  std::string out;
+  for (const char* q = lout; *q; ++q)
+    if (dim[*q] != 1) out.push_back(*q);
+  std::string Ls, Ms, Ns, Ks;
+  for (char ch : out) {
+    bool inx = ox.lab.find(ch) != std::string::npos, iny = oy.lab.find(ch) != std::string::npos;
+    if (inx && iny) Ls.push_back(ch);
+    else if (inx) Ms.push_back(ch);
+    else if (iny) Ns.push_back(ch);
+    else throw Error(-1, "contract: output label not in operands");
+  }
+  for (char ch : ox.lab)
+    if (out.find(ch) == std::string::npos) {
+      if (oy.lab.find(ch) == std::string::npos) throw Error(-1, "contract: label summed in one operand only");
+      Ks.push_back(ch);
+    }
+  for (char ch : oy.lab)
+    if (out.find(ch) == std::string::npos && ox.lab.find(ch) == std::string::npos)
+      throw Error(-1, "contract: label summed in one operand only");
+  int64_t Lsz = 1, Msz = 1, Nsz = 1, Ksz = 1;
+  for (char ch : Ls) Lsz *= dim[ch];
+  for (char ch : Ms) Msz *= dim[ch];
+  for (char ch : Ns) Nsz *= dim[ch];
+  for (char ch : Ks) Ksz *= dim[ch];
+  int nbx = X.bstride ? c.nb : 1;
+  int nby = Y.bstride ? c.nb : 1;
+  bool per_out = X.bstride || Y.bstride;
+
+  // choose the K order: keep whichever operand's order avoids a permute, else the larger's
+  std::string Kx = order_in(ox.lab, Ks), Ky = order_in(oy.lab, Ks);
+  auto x_ok = [&](const std::string& K) {
+    return group_stride(ox, Ls) >= 0 && group_stride(ox, Ms) >= 0 && group_stride(ox, K) >= 0;
+  };
+  auto y_ok = [&](const std::string& K) {
+    return group_stride(oy, Ls) >= 0 && group_stride(oy, Ns) >= 0 && group_stride(oy, K) >= 0;
+  };
+  std::string Kord;
+  int64_t szx = X.size() * nbx, szy = Y.size() * nby;
+  if (x_ok(Kx) && y_ok(Kx)) Kord = Kx;
+  else if (x_ok(Ky) && y_ok(Ky)) Kord = Ky;
+  else if (x_ok(Kx)) Kord = Kx;   // permute Y
+  else if (y_ok(Ky)) Kord = Ky;   // permute X
+  else Kord = (szx >= szy) ? Kx : Ky;
+
+  // materialise operands in GEMM-viewable layouts when needed
+  Tensor Xp, Yp;
+  const Tensor* Xu = &X;
+  const Tensor* Yu = &Y;
+  std::string lxu = lx, lyu = ly;
+  Op oxu = ox, oyu = oy;
+  if (!x_ok(Kord)) {
+    std::string full = Ls + Ms + Kord;
+    // permute needs all labels incl. unit dims: append unit labels at the end
+    std::string src(lx), dst = full;
+    for (char ch : src)
+      if (dst.find(ch) == std::string::npos) dst.push_back(ch);
+    Xp = permute(c, X, lx, dst.c_str(), cx);
+    Xu = &Xp;
+    lxu = dst;
+    oxu = make_op(Xp, dst.c_str(), false);
+  }
+  if (!y_ok(Kord)) {
+    std::string full = Ls + Kord + Ns;
+    std::string src(ly), dst = full;
+    for (char ch : src)
+      if (dst.find(ch) == std::string::npos) dst.push_back(ch);
+    Yp = permute(c, Y, ly, dst.c_str(), cy);
+    Yu = &Yp;
+    lyu = dst;
+    oyu = make_op(Yp, dst.c_str(), false);
+  }
+  // output: GEMM writes [L][M][N]; permute afterwards if lout differs
+  std::string gout = Ls + Ms + Ns;
+  bool direct = (gout == out);
+  Tensor C;
+  std::vector<int> gshape;
+  for (char ch : gout) gshape.push_back(dim[ch]);
+  if (direct) {
+    C = new_tensor_n(c, oshape, per_out ? c.nb : 1);
+  } else {
+    C = new_tensor_n(c, gshape.empty() ? std::vector<int>{1} : gshape, per_out ? c.nb : 1);
+  }
+  if (!per_out) C.bstride = 0;
+
+  GemmDesc g;
+  g.M = (int)Msz;
+  g.N = (int)Nsz;
+  g.K = (int)Ksz;
+  g.A = Xu->p;
+  g.am = group_stride(oxu, Ms);
+  g.ak = group_stride(oxu, Kord);
+  g.conjA = (Xu == &X) ? cx : false;
+  g.B = Yu->p;
+  g.bk = group_stride(oyu, Kord);
+  g.bn = group_stride(oyu, Ns);
+  g.conjB = (Yu == &Y) ? cy : false;
+  g.C = C.p;
+  g.cm = Nsz;
+  if (Ms.empty()) g.am = 0;
+  if (Kord.empty()) { g.ak = 0; g.bk = 0; }
+  if (Ns.empty()) g.bn = 0;
+  int64_t lsx = group_stride(oxu, Ls), lsy = group_stride(oyu, Ls);
+  g.nb2 = (int)Lsz;
+  g.sa2 = Ls.empty() ? 0 : lsx;
+  g.sb2 = Ls.empty() ? 0 : lsy;
+  g.sc2 = Msz * Nsz;
+  g.nb1 = per_out ? c.nb : 1;
+  g.sa1 = Xu->bstride;
+  g.sb1 = Yu->bstride;
+  g.sc1 = C.bstride;
+  if (Ksz == 0 || Msz == 0 || Nsz == 0) { zero(c, C, g.nb1); }
+  // fold the sample batch into M when Y is shared
+  if (g.nb1 > 1 && Yu->bstride == 0 && g.nb2 == 1 && (Ms.empty() ? false : Xu->bstride == Msz * g.am) &&
+      C.bstride == Msz * g.cm) {
+    g.M = (int)(Msz * g.nb1);
+    g.nb1 = 1;
+  }
+  gemm(c, g);
+  if (direct) return C;
+  std::string gl = gout.empty() ? std::string("?") : gout;
+  // permute to requested order (including unit dims)
+  std::string dst(lout), src = gl;
+  for (char ch : dst)
+    if (src.find(ch) == std::string::npos && gl != "?") src.push_back(ch);
+  Tensor Ct = C;
+  Ct.shape.clear();
+  for (char ch : src) Ct.shape.push_back(dim.count(ch) ? dim[ch] : 1);
+  if (gl == "?") { Ct.shape = oshape; return Ct; }
+  Tensor R = permute(c, Ct, src.c_str(), dst.c_str(), false);
+  return R;
+}
+
+}  // namespace tn

@@ -1,0 +1,68 @@
+// tensor.h -- batched complex tensors on the device and the pairwise contraction engine.
+//
+// Every contraction of the method is expressed as one call of
+// contract(): operands are permuted (only when their layout does not already match a
+// GEMM view) and multiplied by a batched complex GEMM (gemm.cu: tcgen05 TF32x3 on
+// sm_100a for large tiles, FP32 SIMT otherwise). The leading "sample" batch of per-sample
+// operands is folded into the GEMM M dimension when the other operand is shared across
+// samples (A_v, the norm environment M), so one launch covers the whole batch.
+#pragma once
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace tn {
+
+struct Tensor {
+  std::shared_ptr<DevBuf> mem;
+  float2* p = nullptr;
+  std::vector<int> shape;
+  int64_t bstride = 0;  // elements between consecutive samples; 0 = shared by all samples
+  int64_t size() const { return prod(shape); }
+  int rank() const { return (int)shape.size(); }
+};
+
+struct Ctx {
+  cudaStream_t stream = nullptr;
+  int gemm_mode = 0;  // 0 auto, 1 SIMT only, 2 tcgen05 whenever legal
+  int nb = 1;         // number of samples in the current batch
+};
+
+// Allocate a tensor: per-sample (nb copies) when per_sample, else shared.
+Tensor new_tensor(Ctx& c, const std::vector<int>& shape, bool per_sample);
+Tensor new_tensor_n(Ctx& c, const std::vector<int>& shape, int nb);  // explicit batch
+void zero(Ctx& c, Tensor& t, int nb);
+
+// out[labels_out] = sum over shared labels of opA(A[la]) * opB(B[lb]); labels are single
+// characters; labels present in A, B and out are element-wise (batched) labels. conj
+// flags conjugate the operand. Per-sample/shared status follows the operands' bstride.
+Tensor contract(Ctx& c, const Tensor& A, const char* la, bool conjA, const Tensor& B,
+                const char* lb, bool conjB, const char* lout);
+
+// Reorder the axes: out labels are a permutation of in labels.
+Tensor permute(Ctx& c, const Tensor& A, const char* la, const char* lout, bool conj = false);
+
+// Plain batched GEMM on strided complex views (row-major C with unit column stride):
+// C[m, n] (+)= sum_k A(m, k) B(k, n), A(m,k) = A[m*am + k*ak], B(k,n) = B[k*bk + n*bn].
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  const float2* A = nullptr;
+  int64_t am = 0, ak = 0;
+  bool conjA = false;
+  const float2* B = nullptr;
+  int64_t bk = 0, bn = 0;
+  bool conjB = false;
+  float2* C = nullptr;
+  int64_t cm = 0;
+  int nb1 = 1, nb2 = 1;
+  int64_t sa1 = 0, sb1 = 0, sc1 = 0, sa2 = 0, sb2 = 0, sc2 = 0;
+  bool accumulate = false;
+};
+void gemm(Ctx& c, const GemmDesc& g);
+
+// Flop accounting of the GEMMs issued (complex MACs), for the roofline report.
+extern double g_cmacs;
+
+}  // namespace tn

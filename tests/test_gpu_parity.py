@@ -1,0 +1,150 @@
+"""GPU <-> oracle parity through the C ABI (libtnsample.so on a B200).
+
+Same seeded inputs on both sides (tninputs), the oracle in complex128 (oracle/), the CUDA
+path in complex64 with FP32/TF32x3 products; tolerances of R16 (tests/parity.py).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from tests.parity import amp_close, compare_samples, oracle_samples
+from tninputs import lattices as L
+from tninputs import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2507_11424_b200 import TNState  # noqa: E402
+from oracle import bmps as B  # noqa: E402
+from oracle import generator as G  # noqa: E402
+from oracle import statevector as SV  # noqa: E402
+
+
+def order_of(rows):
+    return [v for r in rows for v in r]
+
+
+def _run(st, rows, R, u, gemm=0):
+    g = TNState(st)
+    if gemm:
+        g.set_option("gemm", gemm)
+    bits, logq, cond, flags = g.sample(rows, R, u, want_cond=True)
+    return g, bits, logq, cond, flags
+
+
+@pytest.mark.parametrize("gemm", [1, 0])
+def test_exact_regime_square_vs_statevector(gemm):
+    lat = L.square(3, 3)
+    st = S.vidal_like(lat, 2, seed=3, xi=2.0)
+    psi = SV.statevector(st)
+    u = S.uniforms(64, lat.n, 5)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 16, u, gemm)
+    order = order_of(lat.rows)
+    for k in range(len(u)):
+        ref = SV.conditionals(psi, lat.n, order, bits[k])
+        got = [cond[k, v] for v in order]
+        assert np.allclose(got, ref, rtol=1e-4, atol=1e-6), (k, got, ref)
+        idx = int("".join(map(str, bits[k])), 2)
+        lp = math.log(abs(psi[idx]) ** 2 / np.vdot(psi, psi).real)
+        assert abs(logq[k] - lp) <= 1e-4 * max(1, abs(lp))
+    assert abs(g.log_norm(16) - math.log(np.vdot(psi, psi).real)) < 1e-4
+
+
+def test_config1_vs_oracle():
+    lat, st = G.config_state("cfg1")
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, 16)
+    u = S.uniforms(1024, lat.n, 1001)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 16, u)
+    n_ref = 128
+    rb, rl, rc = oracle_samples(P, M, 16, u, n_ref)
+    rep = compare_samples(order_of(lat.rows), u[:n_ref], bits[:n_ref], logq[:n_ref], cond[:n_ref], rb, rl, rc)
+    assert rep["compared"] > 0
+    # U(1): every GPU sample in the domain wall's sector
+    assert (bits.sum(axis=1) == sum(L.domain_wall_bits(lat))).all()
+
+
+def test_config1_truncated_vs_oracle():
+    """Finite chi_env (R=4 < exact rank): q is defined by the fits."""
+    lat, st = G.config_state("cfg1")
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, 4)
+    u = S.uniforms(64, lat.n, 1001)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 4, u)
+    rb, rl, rc = oracle_samples(P, M, 4, u)
+    compare_samples(order_of(lat.rows), u, bits, logq, cond, rb, rl, rc)
+
+
+def test_amplitude_vs_oracle():
+    lat, st = G.config_state("cfg1")
+    P = B.Prepared(st, lat.rows)
+    g = TNState(st)
+    g.prepare(lat.rows, 16)
+    rng = np.random.default_rng(2)
+    x = rng.integers(0, 2, (16, lat.n)).astype(np.uint8)
+    x[:8] = 0
+    for k in range(8):  # magnetisation-sector bitstrings (non-zero amplitudes)
+        ones = rng.choice(lat.n, sum(L.domain_wall_bits(lat)), replace=False)
+        x[k, ones] = 1
+    la, ph = g.amplitude(x, 8)
+    M, logs = B.norm_envs(P, 16)
+    half_lnZ = 0.5 * B.log_norm(P, M, logs)
+    for k in range(len(x)):
+        lr, pr = B.amplitude(P, x[k], 8)
+        assert amp_close(la[k], ph[k], lr, pr, half_lnZ), (k, la[k], lr, ph[k], pr)
+
+
+@pytest.mark.parametrize("lat_name,chi,K,R", [("willow105", 4, 2, 8), ("square4x4", 4, 3, 16)])
+def test_branch_superposition_full_topology(lat_name, chi, K, R):
+    from tests.test_oracle import closed_form_conditionals
+    lat = L.by_name(lat_name)
+    st = S.branch_superposition(lat, chi, K, seed=2)
+    u = S.uniforms(8, lat.n, 77)
+    g, bits, logq, cond, flags = _run(st, lat.rows, R, u)
+    order = order_of(lat.rows)
+    for k in range(len(u)):
+        ref = closed_form_conditionals(st["meta"]["phis"], order, bits[k])
+        got = [cond[k, v] for v in order]
+        for a, b_ in zip(got, ref):
+            assert abs(a - b_) <= 1e-4 * b_ + (1e-6 if b_ < 1e-2 else 0), (k, got, ref)
+
+
+def test_ghz_eagle():
+    lat = L.eagle127()
+    st = S.ghz(lat, chi=2)
+    u = S.uniforms(16, lat.n, 3)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 4, u)
+    for k in range(len(u)):
+        assert len(set(bits[k].tolist())) == 1
+        assert abs(logq[k] - math.log(0.5)) < 1e-5
+
+
+def test_relabelled_rows_same_result():
+    """General row orders through the C ABI: relabelling vertices changes nothing."""
+    lat = L.square(3, 4)
+    st = S.vidal_like(lat, 2, seed=1, xi=2.0)
+    perm = list(np.random.default_rng(0).permutation(lat.n))
+    st2, rows2 = S.relabel(st, lat.rows, perm)
+    u = S.uniforms(16, lat.n, 9)
+    u2 = np.zeros_like(u)
+    for v in range(lat.n):
+        u2[:, perm[v]] = u[:, v]
+    _, b1, l1, c1, _ = _run(st, lat.rows, 16, u)
+    _, b2, l2, c2, _ = _run(st2, rows2, 16, u2)
+    for v in range(lat.n):
+        assert (b1[:, v] == b2[:, perm[v]]).all()
+    assert np.allclose(l1, l2, rtol=1e-5, atol=1e-6)
+
+
+def test_batch_size_determinism():
+    lat, st = G.config_state("cfg1")
+    u = S.uniforms(40, lat.n, 4)
+    g = TNState(st)
+    b1, l1, _, _ = g.sample(lat.rows, 16, u)
+    g.set_option("max_batch", 7)
+    b2, l2, _, _ = g.sample(lat.rows, 16, u)
+    assert (b1 == b2).all() and np.array_equal(l1, l2)

@@ -1,0 +1,232 @@
+"""GPU unit tests of the building blocks (contraction engine, orthonormal bases) against a
+plain numpy reference of the same operation (test-only debug entry points)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2507_11424_b200 import _lib  # noqa: E402
+
+LIB = _lib.lib()
+LIB.tn_debug_last_error.restype = C.c_char_p
+
+
+def rand(rng, shape):
+    return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(np.complex64)
+
+
+def dcontract(A, la, B, lb, lout, nb=1, perA=False, perB=False, cA=False, cB=False, gemm=0):
+    shA = A.shape[1:] if perA else A.shape
+    shB = B.shape[1:] if perB else B.shape
+    A = np.ascontiguousarray(A, dtype=np.complex64)
+    B = np.ascontiguousarray(B, dtype=np.complex64)
+    ref = np.einsum(f"{'Z' if perA else ''}{la},{'Z' if perB else ''}{lb}->{'Z' if (perA or perB) else ''}{lout}",
+                    A.conj() if cA else A, B.conj() if cB else B)
+    out = np.zeros(ref.shape, dtype=np.complex64)
+    sa = (C.c_int * len(shA))(*shA)
+    sb = (C.c_int * len(shB))(*shB)
+    rc = LIB.tn_debug_contract(la.encode(), len(shA), sa, A.ctypes.data_as(C.c_void_p), int(cA), int(perA),
+                               lb.encode(), len(shB), sb, B.ctypes.data_as(C.c_void_p), int(cB), int(perB),
+                               lout.encode(), nb, out.ctypes.data_as(C.c_void_p), C.c_int64(out.size), gemm)
+    assert rc == 0, LIB.tn_debug_last_error()
+    return out, ref
+
+
+LIB.tn_debug_contract.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_char_p,
+                                  C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_int,
+                                  C.c_void_p, C.c_int64, C.c_int]
+LIB.tn_debug_orth.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+
+
+def close(a, b, tol=2e-5):
+    return np.linalg.norm(a - b) <= tol * max(1e-30, np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("gemm", [1, 0])
+@pytest.mark.parametrize("case", [
+    ("ab", (37, 29), "bc", (29, 41), "ac"),
+    ("ab", (37, 29), "cb", (41, 29), "ca"),
+    ("xmy", (5, 7, 3), "mun", (7, 4, 6), "xyun"),
+    ("xyun", (5, 3, 4, 6), "upyr", (4, 9, 3, 2), "xnpr"),
+    ("xnpr", (5, 6, 9, 2), "znr", (8, 6, 2), "xpz"),
+    ("asZeD", (3, 2, 4, 5, 6), "AsDZ", (7, 2, 6, 4), "saeA"),
+    ("xeab", (3, 4, 2, 2), "edDf", (4, 3, 3, 5), "xabdDf"),
+])
+def test_contract_shared(case, gemm):
+    rng = np.random.default_rng(0)
+    la, sa, lb, sb, lo = case
+    out, ref = dcontract(rand(rng, sa), la, rand(rng, sb), lb, lo, gemm=gemm)
+    assert close(out, ref)
+
+
+@pytest.mark.parametrize("gemm", [1, 0])
+def test_contract_batched_and_conj(gemm):
+    rng = np.random.default_rng(1)
+    nb = 5
+    A = rand(rng, (nb, 6, 7, 3))
+    B = rand(rng, (7, 3, 4))
+    out, ref = dcontract(A, "xmy", B, "myn", "xn", nb=nb, perA=True, gemm=gemm)
+    assert close(out, ref)
+    out, ref = dcontract(B, "myn", A, "xmy", "nx", nb=nb, perB=True, cA=True, gemm=gemm)
+    assert close(out, ref)
+    B2 = rand(rng, (nb, 7, 3, 4))
+    out, ref = dcontract(A, "xmy", B2, "myn", "nx", nb=nb, perA=True, perB=True, cB=True, gemm=gemm)
+    assert close(out, ref)
+    # element-wise (batched) label + unit dims
+    A3 = rand(rng, (nb, 2, 3, 1, 4))
+    B3 = rand(rng, (nb, 5, 2, 1, 4))
+    out, ref = dcontract(A3, "saez", B3, "Asuz", "saeA", nb=nb, perA=True, perB=True, cB=True, gemm=gemm)
+    assert close(out, ref)
+
+
+def test_contract_large_k():
+    rng = np.random.default_rng(2)
+    out, ref = dcontract(rand(rng, (130, 1000)), "ak", rand(rng, (1000, 70)), "kb", "ab")
+    assert close(out, ref, 1e-5)
+
+
+def _orth(X, transpose=False):
+    nb = X.shape[0]
+    if transpose:
+        n, m = X.shape[1], X.shape[2]
+    else:
+        m, n = X.shape[1], X.shape[2]
+    X = np.ascontiguousarray(X, dtype=np.complex64)
+    Q = np.zeros_like(X)
+    Cm = np.zeros((nb, n, n), dtype=np.complex64)
+    rc = LIB.tn_debug_orth(m, n, nb, X.ctypes.data_as(C.c_void_p), Q.ctypes.data_as(C.c_void_p),
+                           Cm.ctypes.data_as(C.c_void_p), int(transpose))
+    assert rc == 0, LIB.tn_debug_last_error()
+    return Q, Cm
+
+
+@pytest.mark.parametrize("m,n", [(64, 16), (300, 128), (40, 40), (8192, 128)])
+def test_orth_full_rank(m, n):
+    rng = np.random.default_rng(3)
+    X = rand(rng, (3, m, n)) * np.logspace(0, -4, n)[None, None, :]
+    Q, Cm = _orth(X)
+    for b in range(3):
+        q = Q[b].astype(np.complex128)
+        assert np.abs(q.conj().T @ q - np.eye(n)).max() < 1e-5
+        # span: X = Q (Q^H X)
+        x = X[b].astype(np.complex128)
+        assert np.linalg.norm(x - q @ (q.conj().T @ x)) < 1e-5 * np.linalg.norm(x)
+        assert np.linalg.norm(x - q @ Cm[b]) < 1e-5 * np.linalg.norm(x)
+
+
+def test_orth_rank_deficient():
+    rng = np.random.default_rng(4)
+    m, n, r = 200, 32, 5
+    X = (rand(rng, (2, m, r)) @ rand(rng, (2, r, n))).astype(np.complex64)
+    X[1] = 0
+    Q, _ = _orth(X)
+    for b in range(2):
+        q = Q[b].astype(np.complex128)
+        assert np.abs(q.conj().T @ q - np.eye(n)).max() < 1e-5
+        x = X[b].astype(np.complex128)
+        assert np.linalg.norm(x - q @ (q.conj().T @ x)) <= 1e-5 * max(1e-30, np.linalg.norm(x))
+
+
+def test_orth_rows():
+    rng = np.random.default_rng(5)
+    X = rand(rng, (2, 24, 300))  # rows orthonormalised (right_orth)
+    Q, Cm = _orth(X, transpose=True)
+    for b in range(2):
+        q = Q[b].astype(np.complex128)
+        assert np.abs(q @ q.conj().T - np.eye(24)).max() < 1e-5
+        x = X[b].astype(np.complex128)
+        # X = C^H Q
+        assert np.linalg.norm(x - Cm[b].conj().T @ q) < 1e-5 * np.linalg.norm(x)
+
+
+LIB.tn_debug_fit.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                             C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.c_int64,
+                             C.c_void_p, C.c_void_p, C.c_int]
+
+
+def gpu_fit(strip, R, tag=1, b1=1, nh=2, gemm=0):
+    from oracle import bmps as B
+    W = strip.W
+    dbl = strip.kind == "double"
+    keep = []
+    tshape = np.zeros(4 * W, dtype=np.int32)
+    tptr = (C.c_void_p * W)()
+    tb = np.zeros(W, dtype=np.int32)
+    mshape = np.zeros(5 * W, dtype=np.int32)
+    mptr = (C.c_void_p * W)()
+    for j in range(W):
+        t = np.ascontiguousarray(strip.tops[j], dtype=np.complex64)
+        keep.append(t)
+        tshape[4 * j: 4 * j + t.ndim] = t.shape
+        tptr[j] = t.ctypes.data
+        tb[j] = t.shape[0]
+        m = np.ascontiguousarray(strip.mats[j], dtype=np.complex64)
+        keep.append(m)
+        mshape[5 * j: 5 * j + m.ndim] = m.shape
+        mptr[j] = m.ctypes.data
+    outc = np.asarray(strip.out, dtype=np.int32)
+    cap = 1 << 22
+    out = np.zeros(cap, dtype=np.complex64)
+    shapes = np.zeros(4 * W, dtype=np.int32)
+    logn = np.zeros(1)
+    K = LIB.tn_debug_fit(int(dbl), W, tshape.ctypes.data, tptr, tb.ctypes.data, mshape.ctypes.data, mptr,
+                         outc.ctypes.data, R, tag, b1, nh, B.DEFAULT_SEED, out.ctypes.data, cap,
+                         shapes.ctypes.data, logn.ctypes.data, gemm)
+    assert K >= 0, LIB.tn_debug_last_error()
+    sites, off = [], 0
+    for k in range(K):
+        sh = [int(x) for x in shapes[4 * k: 4 * k + 4] if x]
+        size = int(np.prod(sh))
+        sites.append(out[off: off + size].reshape(sh).astype(np.complex128))
+        off += size
+    return sites, float(logn[0])
+
+
+def _dense(sites):
+    v = np.ones((1, 1))
+    for s in sites:
+        s = s.reshape(s.shape[0], -1, s.shape[-1])
+        v = np.einsum("Pa,apb->Ppb", v, s).reshape(-1, s.shape[-1])
+    return v.reshape(-1)
+
+
+@pytest.mark.parametrize("R", [64, 3])
+@pytest.mark.parametrize("gemm", [1, 0])
+def test_fit_single_matches_oracle(R, gemm):
+    import math
+    from oracle import bmps as B
+    from tests.test_oracle import _random_strip
+    rng = np.random.default_rng(7)
+    strip = _random_strip(rng, W=5, chi=3, mu=3)
+    so, lo = B.fit(strip, R=R, tag=1, b1=2)
+    sg, lg = gpu_fit(strip, R, tag=1, b1=2, gemm=gemm)
+    ref = _dense(so) * math.exp(lo)
+    got = _dense(sg) * math.exp(lg)
+    assert np.linalg.norm(got - ref) <= 1e-4 * np.linalg.norm(ref)
+
+
+def test_fit_double_matches_oracle():
+    import math
+    from oracle import bmps as B
+    from tninputs import lattices as L
+    from tninputs import synthetic as S
+    lat = L.square(3, 3)
+    st = S.vidal_like(lat, 2, seed=3, xi=2.0)
+    P = B.Prepared(st, lat.rows)
+    for R in (16, 3):
+        M, logs = B.norm_envs(P, R)
+        # fit of row 1 (0-based) with M[1] from below, as in norm_envs
+        row = P.rows[1]
+        tops = B._tops_for_row(P, row, M[1], "down", "double")
+        strip = B.Strip("double", tops, [P.A[v] for v in row], [P.has(v, "up") for v in row])
+        so, lo = B.fit(strip, R, B.TAG_M, 2)
+        sg, lg = gpu_fit(strip, R, tag=B.TAG_M, b1=2)
+        ref = _dense(so) * math.exp(lo)
+        got = _dense(sg) * math.exp(lg)
+        assert np.linalg.norm(got - ref) <= 1e-4 * np.linalg.norm(ref), R
