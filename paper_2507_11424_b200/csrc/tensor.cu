@@ -457,6 +457,7 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
   g.sa1 = Xu->bstride;
   g.sb1 = Yu->bstride;
   g.sc1 = C.bstride;
+  g.work_per_sample = Msz * Nsz * Ksz * Lsz;
   if (Ksz == 0 || Msz == 0 || Nsz == 0) { zero(c, C, g.nb1); }
   // fold the sample batch into M when Y is shared
   if (g.nb1 > 1 && Yu->bstride == 0 && g.nb2 == 1 && (Ms.empty() ? false : Xu->bstride == Msz * g.am) &&

@@ -59,6 +59,7 @@ struct GemmDesc {
   int nb1 = 1, nb2 = 1;
   int64_t sa1 = 0, sb1 = 0, sc1 = 0, sa2 = 0, sb2 = 0, sc2 = 0;
   bool accumulate = false;
+  int64_t work_per_sample = 0;  // complex MACs of one sample (kernel choice must not depend on batch)
 };
 void gemm(Ctx& c, const GemmDesc& g);
 

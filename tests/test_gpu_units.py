@@ -48,7 +48,7 @@ def close(a, b, tol=2e-5):
     return np.linalg.norm(a - b) <= tol * max(1e-30, np.linalg.norm(b))
 
 
-@pytest.mark.parametrize("gemm", [1, 0])
+@pytest.mark.parametrize("gemm", [1, 0, 2])
 @pytest.mark.parametrize("case", [
     ("ab", (37, 29), "bc", (29, 41), "ac"),
     ("ab", (37, 29), "cb", (41, 29), "ca"),
@@ -65,7 +65,7 @@ def test_contract_shared(case, gemm):
     assert close(out, ref)
 
 
-@pytest.mark.parametrize("gemm", [1, 0])
+@pytest.mark.parametrize("gemm", [1, 0, 2])
 def test_contract_batched_and_conj(gemm):
     rng = np.random.default_rng(1)
     nb = 5
@@ -197,7 +197,7 @@ def _dense(sites):
 
 
 @pytest.mark.parametrize("R", [64, 3])
-@pytest.mark.parametrize("gemm", [1, 0])
+@pytest.mark.parametrize("gemm", [1, 0, 2])
 def test_fit_single_matches_oracle(R, gemm):
     import math
     from oracle import bmps as B
