@@ -272,6 +272,99 @@ __global__ void prep_a_kernel(const float2* __restrict__ A, int64_t am, int64_t 
   }
 }
 
+__device__ __forceinline__ int64_t view_off(const View4& v, int64_t idx) {
+  int64_t off = 0;
+#pragma unroll
+  for (int d = 3; d >= 0; --d) {
+    if (d < v.rank) {
+      const int64_t q = idx / v.dims[d];
+      off += (idx - q * v.dims[d]) * v.str[d];
+      idx = q;
+    }
+  }
+  return off;
+}
+
+// Tiled gather of an operand X(r, k) (r = row index M or N, k = K index; both compound,
+// View4) into TF32 hi/lo planes. 32 rows x 32 complex k per block through shared memory:
+// loads run along whichever side is contiguous in memory (k_fast), stores along the plane's
+// K axis. kind 0: A planes [z][Rp][Krp], element (r, 2k+c) = (Re, Im)[c];
+// kind 1: B_r^T planes [z][2*Rp'][Krp], rows 2r = (Re b, -Im b), 2r+1 = (Im b, Re b).
+struct PrepArgs {
+  const float2* X;
+  View4 vr, vk;
+  int conj, nb2;
+  int64_t s1, s2;
+  int z0, R, K, Rrows, Krp;  // Rrows: padded plane rows (A: Mp; B: Nrp)
+  int k_fast;
+  float* hi;
+  float* lo;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
+  __shared__ float2 tile[32][33];
+  __shared__ int64_t roff[32], koff[32];
+  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+  const int zz = blockIdx.z;
+  const int z = a.z0 + zz;
+  const int b1 = z / a.nb2, b2 = z - b1 * a.nb2;
+  const float2* base = a.X + b1 * a.s1 + b2 * a.s2;
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  if (t < 32) roff[t] = (r0 + t < a.R) ? view_off(a.vr, r0 + t) : -1;
+  else if (t < 64) koff[t - 32] = (k0 + t - 32 < a.K) ? view_off(a.vk, k0 + t - 32) : -1;
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    const int rr = a.k_fast ? j : tx, kk = a.k_fast ? tx : j;
+    const int64_t ro = roff[rr], ko = koff[kk];
+    float2 v = make_float2(0.f, 0.f);
+    if (ro >= 0 && ko >= 0) v = base[ro + ko];
+    if (a.conj) v.y = -v.y;
+    tile[rr][kk] = v;
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)a.Rrows * a.Krp;
+  if (KIND == 0) {
+    for (int j = ty; j < 32; j += 8) {
+      const int r = r0 + j;
+      if (r >= a.Rrows) continue;
+      float* hrow = a.hi + zz * plane + (int64_t)r * a.Krp;
+      float* lrow = a.lo + zz * plane + (int64_t)r * a.Krp;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kr2 = tx + 32 * h;  // 0..63 real columns of this tile
+        const int kr = 2 * k0 + kr2;
+        if (kr >= a.Krp) continue;
+        const float2 v = tile[j][kr2 >> 1];
+        const float x = (kr2 & 1) ? v.y : v.x;
+        const float hv = tf32_trunc(x);
+        hrow[kr] = hv;
+        lrow[kr] = x - hv;
+      }
+    }
+  } else {
+    for (int j = ty; j < 64; j += 8) {  // 64 plane rows = 32 complex columns of B
+      const int rr = j >> 1, par = j & 1;
+      const int row = 2 * r0 + j;
+      if (row >= a.Rrows) continue;
+      float* hrow = a.hi + zz * plane + (int64_t)row * a.Krp;
+      float* lrow = a.lo + zz * plane + (int64_t)row * a.Krp;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kr2 = tx + 32 * h;
+        const int kr = 2 * k0 + kr2;
+        if (kr >= a.Krp) continue;
+        const float2 b = tile[rr][kr2 >> 1];
+        const int sel = (par << 1) | (kr2 & 1);
+        const float x = sel == 0 ? b.x : (sel == 1 ? -b.y : (sel == 2 ? b.y : b.x));
+        const float hv = tf32_trunc(x);
+        hrow[kr] = hv;
+        lrow[kr] = x - hv;
+      }
+    }
+  }
+}
+
 // B_r^T hi/lo planes: [z][Nrp][Krp]; row 2n = (Re b, -Im b), row 2n+1 = (Im b, Re b)
 __global__ void prep_b_kernel(const float2* __restrict__ B, int64_t bk, int64_t bn, int conj, int nb2, int64_t sb1,
                               int64_t sb2, int z0, int N, int K, int Nrp, int Krp, float* __restrict__ hi,
@@ -333,10 +426,16 @@ inline int rup(int x, int m) { return (x + m - 1) / m * m; }
 // depends on per-sample shapes only, so results do not depend on the batch size.
 static const double kTcMinWork = 1 << 20;
 
-bool gemm_tc(Ctx& c, const GemmDesc& g) {
+bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per_sample) {
   if (c.gemm_mode == 1) return false;
-  double work = g.work_per_sample > 0 ? (double)g.work_per_sample : (double)g.M * g.N * g.K;
-  if (c.gemm_mode != 2 && (work < kTcMinWork || g.N < 32 || g.K < 8)) return false;
+  if (M <= 0 || N <= 0 || K <= 0) return false;
+  if (c.gemm_mode == 2) return true;
+  double work = work_per_sample > 0 ? (double)work_per_sample : (double)M * N * K;
+  return work >= kTcMinWork && N >= 32 && K >= 8;
+}
+
+bool gemm_tc(Ctx& c, const GemmDesc& g) {
+  if (!tc_eligible(c, g.M, g.N, g.K, g.work_per_sample)) return false;
   static bool attr = false;
   if (!attr) {
     TN_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
@@ -350,11 +449,33 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
   // B planes (once, or per batch element)
   const int nzb = b_batched ? nbz : 1;
   DevBuf bh((size_t)nzb * Nrp * Krp * 4, c.stream), bl((size_t)nzb * Nrp * Krp * 4, c.stream);
+  auto simple = [](int64_t dim, int64_t stride) {
+    View4 v;
+    v.rank = 1;
+    v.dims[0] = (int)dim;
+    v.str[0] = stride;
+    return v;
+  };
+  auto inner_unit = [](const View4& v) { return v.rank > 0 && v.str[v.rank - 1] == 1; };
   {
-    int64_t tot = (int64_t)nzb * Nrp * Krp;
-    unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 32);
-    prep_b_kernel<<<blocks, 256, 0, c.stream>>>(g.B, g.bk, g.bn, g.conjB, g.nb2, g.sb1, g.sb2, 0, g.N, g.K, Nrp, Krp,
-                                                bh.as<float>(), bl.as<float>(), nzb);
+    PrepArgs a;
+    a.X = g.B;
+    a.vr = g.vbn.rank ? g.vbn : simple(g.N, g.bn);
+    a.vk = g.vbk.rank ? g.vbk : simple(g.K, g.bk);
+    a.conj = g.conjB;
+    a.nb2 = g.nb2;
+    a.s1 = b_batched ? g.sb1 : 0;
+    a.s2 = b_batched ? g.sb2 : 0;
+    a.z0 = 0;
+    a.R = g.N;
+    a.K = g.K;
+    a.Rrows = Nrp;
+    a.Krp = Krp;
+    a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
+    a.hi = bh.as<float>();
+    a.lo = bl.as<float>();
+    dim3 grid(ceil_div(Krp / 2, 32), Nrp / 64, nzb);
+    prep_tiled_kernel<1><<<grid, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
   }
   CUtensorMap mbh = make_map(bh.as<float>(), Krp, Nrp, nzb, TC_BN);
@@ -365,11 +486,27 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
   DevBuf ah((size_t)zc * per_z * 4, c.stream), al((size_t)zc * per_z * 4, c.stream);
   for (int z0 = 0; z0 < nbz; z0 += zc) {
     const int nz = std::min(zc, nbz - z0);
-    int64_t tot = (int64_t)nz * per_z;
-    unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 32);
-    prep_a_kernel<<<blocks, 256, 0, c.stream>>>(g.A, g.am, g.ak, g.conjA, g.nb2, g.sa1, g.sa2, z0, g.M, g.K, Mp, Krp,
-                                                ah.as<float>(), al.as<float>(), nz);
-    TN_LAUNCHED();
+    {
+      PrepArgs a;
+      a.X = g.A;
+      a.vr = g.vam.rank ? g.vam : simple(g.M, g.am);
+      a.vk = g.vak.rank ? g.vak : simple(g.K, g.ak);
+      a.conj = g.conjA;
+      a.nb2 = g.nb2;
+      a.s1 = g.sa1;
+      a.s2 = g.sa2;
+      a.z0 = z0;
+      a.R = g.M;
+      a.K = g.K;
+      a.Rrows = Mp;
+      a.Krp = Krp;
+      a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
+      a.hi = ah.as<float>();
+      a.lo = al.as<float>();
+      dim3 grid(ceil_div(Krp / 2, 32), Mp / 32, nz);
+      prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
+      TN_LAUNCHED();
+    }
     CUtensorMap mah = make_map(ah.as<float>(), Krp, Mp, nz, TC_BM);
     CUtensorMap mal = make_map(al.as<float>(), Krp, Mp, nz, TC_BM);
     TcParams p;

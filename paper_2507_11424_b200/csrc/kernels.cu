@@ -202,6 +202,7 @@ void hash_init(Ctx& c, Tensor& o, int nb, uint64_t seed, int tag, int b1, int k)
 }
 
 void normalize(Ctx& c, Tensor& t, int nb, double* logn, bool acc) {
+  ProfScope ps(P_MISC, c.stream);
   int n = t.bstride ? nb : 1;
   int64_t size = t.size();
   int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(256, size / 4096));
@@ -226,6 +227,7 @@ Tensor sum2(Ctx& c, const Tensor& t) {
 }
 
 void tail_draw(Ctx& c, const Tensor& L, const Tensor& Rs, int nb, const TailOut& o) {
+  ProfScope ps(P_TAIL, c.stream);
   int64_t size = L.size();
   if (Rs.size() != 2 * size) throw Error(-1, "tail_draw: size mismatch");
   int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(512, size / 8192));

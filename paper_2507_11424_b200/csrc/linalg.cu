@@ -354,6 +354,7 @@ void orthonormalize(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, in
   int m = X.m, n = X.n;
   if (n == 0 || nb == 0) return;
   if (m < n) throw Error(-1, "orthonormalize: more columns than rows");
+  ProfScope ps(P_ORTH, c.stream);
   size_t nn = (size_t)n * n * nb;
   DevBuf G(nn * sizeof(double2), c.stream), W(nn * sizeof(double2), c.stream);
   DevBuf perm((size_t)n * nb * sizeof(int), c.stream), rank((size_t)nb * sizeof(int), c.stream);

@@ -68,8 +68,79 @@ __global__ void permute_kernel(const float2* __restrict__ in, float2* __restrict
   }
 }
 
-// 2D tiled transpose for the common case "swap two compound groups" is left for later; the
-// generic kernel above is L2-assisted and HBM-bound on the large ladder intermediates.
+// Row copy: the innermost output axis is contiguous in the input as well. One warp per output
+// row (all axes but the last), lanes across the row: coalesced on both sides.
+__global__ void permute_rows_kernel(const float2* __restrict__ in, float2* __restrict__ out, PermArgs a) {
+  const int64_t L = a.dims[a.rank - 1];
+  const int64_t rows_per = a.size / L, rows = rows_per * a.nb;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = w0; row < rows; row += nw) {
+    const int64_t b = row / rows_per;
+    int64_t rem = row - b * rows_per, off = 0;
+    for (int d = a.rank - 2; d >= 0; --d) {
+      const int64_t q = rem / a.dims[d];
+      off += (rem - q * a.dims[d]) * a.istride[d];
+      rem = q;
+    }
+    const float2* src = in + b * a.ibs + off;
+    float2* dst = out + b * a.obs + (row - b * rows_per) * L;
+    for (int64_t l = lane; l < L; l += 32) {
+      float2 v = src[l];
+      if (a.conj) v.y = -v.y;
+      dst[l] = v;
+    }
+  }
+}
+
+// Tiled transpose: output axis `kin` is the input's contiguous axis, the last output axis is
+// strided in the input. 32x32 tiles through shared memory; every other axis (and the
+// sample) is a batch coordinate of the grid.
+struct Perm2 {
+  PermArgs a;
+  int kin;                 // output axis with input stride 1
+  int64_t ostride[8];      // output strides (row-major of the output dims)
+  int64_t nother;          // product of the other axes
+  int ntk, ntl;            // tiles along kin and along the last axis
+};
+
+__global__ void __launch_bounds__(256) permute_tile_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                                                           Perm2 p) {
+  __shared__ float2 tile[32][33];
+  const PermArgs& a = p.a;
+  const int last = a.rank - 1;
+  const int64_t dk = a.dims[p.kin], dl = a.dims[last];
+  const int t = blockIdx.x, tk = t % p.ntk, tl = t / p.ntk;
+  const int64_t bb = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
+  if (bb >= p.nother * a.nb) return;
+  const int64_t b = bb / p.nother;
+  int64_t rem = bb - b * p.nother, ioff = 0, ooff = 0;
+  for (int d = last - 1; d >= 0; --d) {
+    if (d == p.kin) continue;
+    const int64_t q = rem / a.dims[d];
+    const int64_t idx = rem - q * a.dims[d];
+    ioff += idx * a.istride[d];
+    ooff += idx * p.ostride[d];
+    rem = q;
+  }
+  const float2* src = in + b * a.ibs + ioff;
+  float2* dst = out + b * a.obs + ooff;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int j = ty; j < 32; j += 8) {
+    const int64_t l = (int64_t)tl * 32 + j, k = (int64_t)tk * 32 + tx;
+    if (l < dl && k < dk) tile[j][tx] = src[k + l * a.istride[last]];
+  }
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    const int64_t k = (int64_t)tk * 32 + j, l = (int64_t)tl * 32 + tx;
+    if (l < dl && k < dk) {
+      float2 v = tile[tx][j];
+      if (a.conj) v.y = -v.y;
+      dst[k * p.ostride[p.kin] + l] = v;
+    }
+  }
+}
 
 static std::vector<int64_t> strides_of(const std::vector<int>& shape) {
   std::vector<int64_t> s(shape.size());
@@ -100,14 +171,30 @@ Tensor permute(Ctx& c, const Tensor& A, const char* la, const char* lout, bool c
       istr.push_back(st[j]);
     }
   }
-  if (dims.size() > 8) throw Error(-1, "permute: rank > 8");
+  // merge output axes that are also adjacent (and in order) in the input
+  std::vector<int64_t> md, ms;
+  for (size_t i = 0; i < dims.size(); ++i) {
+    if (!md.empty() && ms.back() == istr[i] * dims[i]) {
+      md.back() *= dims[i];
+      ms.back() = istr[i];
+    } else {
+      md.push_back(dims[i]);
+      ms.push_back(istr[i]);
+    }
+  }
+  if (md.size() > 8) throw Error(-1, "permute: rank > 8");
   int nb = A.bstride ? c.nb : 1;
   Tensor out = new_tensor_n(c, oshape, nb);
   if (!A.bstride) out.bstride = 0;
-  a.rank = (int)dims.size();
+  a.rank = (int)md.size();
   for (int i = 0; i < a.rank; ++i) {
-    a.dims[i] = dims[i];
-    a.istride[i] = istr[i];
+    a.dims[i] = md[i];
+    a.istride[i] = ms[i];
+  }
+  if (a.rank == 0) {
+    a.rank = 1;
+    a.dims[0] = 1;
+    a.istride[0] = 1;
   }
   a.size = A.size();
   a.ibs = A.bstride;
@@ -116,8 +203,36 @@ Tensor permute(Ctx& c, const Tensor& A, const char* la, const char* lout, bool c
   a.conj = conj;
   int64_t total = a.size * nb;
   if (total == 0) return out;
-  unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
-  permute_kernel<<<blocks, 256, 0, c.stream>>>(A.p, out.p, a);
+  ProfScope ps(P_PERMUTE, c.stream);
+  const int last = a.rank - 1;
+  int kin = -1;
+  for (int i = 0; i < a.rank; ++i)
+    if (a.istride[i] == 1) kin = i;
+  if (kin == last && a.dims[last] >= 16) {
+    int64_t rows = total / a.dims[last];
+    unsigned blocks = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 64);
+    permute_rows_kernel<<<blocks, 256, 0, c.stream>>>(A.p, out.p, a);
+  } else if (kin >= 0 && kin != last && a.dims[last] >= 8 && a.dims[kin] >= 8) {
+    Perm2 p;
+    p.a = a;
+    p.kin = kin;
+    int64_t acc = 1;
+    for (int i = last; i >= 0; --i) {
+      p.ostride[i] = acc;
+      acc *= a.dims[i];
+    }
+    p.nother = a.size / (a.dims[kin] * a.dims[last]);
+    p.ntk = (int)((a.dims[kin] + 31) / 32);
+    p.ntl = (int)((a.dims[last] + 31) / 32);
+    int64_t nbat = p.nother * nb;
+    unsigned gy = (unsigned)std::min<int64_t>(nbat, 65535);
+    unsigned gz = (unsigned)((nbat + gy - 1) / gy);
+    dim3 grid((unsigned)(p.ntk * p.ntl), gy, gz);
+    permute_tile_kernel<<<grid, 256, 0, c.stream>>>(A.p, out.p, p);
+  } else {
+    unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    permute_kernel<<<blocks, 256, 0, c.stream>>>(A.p, out.p, a);
+  }
   TN_LAUNCHED();
   return out;
 }
@@ -237,7 +352,11 @@ void gemm(Ctx& c, const GemmDesc& g) {
     }
     return;
   }
-  if (c.gemm_mode != 1 && gemm_tc(c, g)) return;
+  {
+    ProfScope ps(P_GEMM_TC, c.stream);
+    if (c.gemm_mode != 1 && gemm_tc(c, g)) return;
+  }
+  ProfScope ps(P_GEMM_SIMT, c.stream);
   int64_t nbz = (int64_t)g.nb1 * g.nb2;
   if (nbz > 65535) {
     // split the outer batch into chunks
@@ -391,13 +510,50 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
   else if (y_ok(Ky)) Kord = Ky;   // permute X
   else Kord = (szx >= szy) ? Kx : Ky;
 
+  // Tensor-core GEMMs gather their operands from any multi-axis layout while splitting them
+  // into TF32 planes, so no permute is needed on that path.
+  GemmDesc gv;
+  bool views = false;
+  static const bool no_views = getenv("TN_NOVIEWS") != nullptr;
+  if (!no_views && (!x_ok(Kord) || !y_ok(Kord)) && tc_eligible(c, Msz, Nsz, Ksz, Msz * Nsz * Ksz * Lsz) &&
+      group_stride(ox, Ls) >= 0 && group_stride(oy, Ls) >= 0) {
+    auto mkview = [](const Op& o, const std::string& grp, View4& v) {
+      std::vector<int64_t> d, s;
+      for (char ch : grp) {
+        size_t p = o.lab.find(ch);
+        int64_t dd = o.dims[p], ss = o.str[p];
+        if (!d.empty() && s.back() == ss * dd) {
+          d.back() *= dd;
+          s.back() = ss;
+        } else {
+          d.push_back(dd);
+          s.push_back(ss);
+        }
+      }
+      if (d.size() > 4) return false;
+      if (d.empty()) {
+        d.push_back(1);
+        s.push_back(0);
+      }
+      v.rank = (int)d.size();
+      for (int i = 0; i < v.rank; ++i) {
+        v.dims[i] = (int)d[i];
+        v.str[i] = s[i];
+      }
+      return true;
+    };
+    std::string Kv = Kx;
+    views = mkview(ox, Ms, gv.vam) && mkview(ox, Kv, gv.vak) && mkview(oy, Kv, gv.vbk) && mkview(oy, Ns, gv.vbn);
+  }
   // materialise operands in GEMM-viewable layouts when needed
   Tensor Xp, Yp;
   const Tensor* Xu = &X;
   const Tensor* Yu = &Y;
   std::string lxu = lx, lyu = ly;
   Op oxu = ox, oyu = oy;
-  if (!x_ok(Kord)) {
+  if (views) {
+    // gather path: no operand permutes
+  } else if (!x_ok(Kord)) {
     std::string full = Ls + Ms + Kord;
     // permute needs all labels incl. unit dims: append unit labels at the end
     std::string src(lx), dst = full;
@@ -408,7 +564,7 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
     lxu = dst;
     oxu = make_op(Xp, dst.c_str(), false);
   }
-  if (!y_ok(Kord)) {
+  if (!views && !y_ok(Kord)) {
     std::string full = Ls + Kord + Ns;
     std::string src(ly), dst = full;
     for (char ch : src)
@@ -459,9 +615,28 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
   g.sc1 = C.bstride;
   g.work_per_sample = Msz * Nsz * Ksz * Lsz;
   if (Ksz == 0 || Msz == 0 || Nsz == 0) { zero(c, C, g.nb1); }
-  // fold the sample batch into M when Y is shared
-  if (g.nb1 > 1 && Yu->bstride == 0 && g.nb2 == 1 && (Ms.empty() ? false : Xu->bstride == Msz * g.am) &&
-      C.bstride == Msz * g.cm) {
+  if (views) {
+    g.vam = gv.vam;
+    g.vak = gv.vak;
+    g.vbk = gv.vbk;
+    g.vbn = gv.vbn;
+    g.conjA = cx;
+    g.conjB = cy;
+    // fold the sample batch into M (outermost M axis) when Y is shared
+    if (g.nb1 > 1 && Y.bstride == 0 && g.nb2 == 1 && g.vam.rank < 4 && C.bstride == Msz * g.cm) {
+      for (int i = g.vam.rank; i > 0; --i) {
+        g.vam.dims[i] = g.vam.dims[i - 1];
+        g.vam.str[i] = g.vam.str[i - 1];
+      }
+      g.vam.dims[0] = g.nb1;
+      g.vam.str[0] = X.bstride;
+      g.vam.rank += 1;
+      g.M = (int)(Msz * g.nb1);
+      g.nb1 = 1;
+    }
+  } else if (g.nb1 > 1 && Yu->bstride == 0 && g.nb2 == 1 && (Ms.empty() ? false : Xu->bstride == Msz * g.am) &&
+             C.bstride == Msz * g.cm) {
+    // fold the sample batch into M when Y is shared
     g.M = (int)(Msz * g.nb1);
     g.nb1 = 1;
   }

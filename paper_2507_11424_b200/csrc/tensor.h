@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "common.h"
+#include "prof.h"
 
 namespace tn {
 
@@ -44,9 +45,19 @@ Tensor contract(Ctx& c, const Tensor& A, const char* la, bool conjA, const Tenso
 // Reorder the axes: out labels are a permutation of in labels.
 Tensor permute(Ctx& c, const Tensor& A, const char* la, const char* lout, bool conj = false);
 
+// Compound index of up to 4 axes (outer -> inner) with arbitrary element strides.
+struct View4 {
+  int rank = 0;
+  int dims[4] = {1, 1, 1, 1};
+  int64_t str[4] = {0, 0, 0, 0};
+};
+
 // Plain batched GEMM on strided complex views (row-major C with unit column stride):
 // C[m, n] (+)= sum_k A(m, k) B(k, n), A(m,k) = A[m*am + k*ak], B(k,n) = B[k*bk + n*bn].
+// When the v* views are set (rank > 0) they replace the single strides (tensor-core path
+// only): the operand preparation gathers straight from the multi-axis layout.
 struct GemmDesc {
+  View4 vam, vak, vbk, vbn;
   int M = 0, N = 0, K = 0;
   const float2* A = nullptr;
   int64_t am = 0, ak = 0;
@@ -62,6 +73,8 @@ struct GemmDesc {
   int64_t work_per_sample = 0;  // complex MACs of one sample (kernel choice must not depend on batch)
 };
 void gemm(Ctx& c, const GemmDesc& g);
+// Whether gemm() will route a GEMM of this per-sample shape to the tensor cores.
+bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per_sample);
 
 // Flop accounting of the GEMMs issued (complex MACs), for the roofline report.
 extern double g_cmacs;

@@ -230,7 +230,8 @@ Envs& norm_envs(tn_state* st, Layout& L, int R) {
   int nbr = (int)L.rows.size();
   E.M.assign(nbr, {});
   E.logs.assign(nbr, 0.0);
-  DevBuf logd(sizeof(double), c.stream);
+  DevBuf logd(sizeof(double) * nbr, c.stream);
+  TN_CUDA(cudaMemsetAsync(logd.p, 0, sizeof(double) * nbr, c.stream));
   for (int b = nbr - 1; b >= 1; --b) {
     DStrip s;
     s.dbl = true;
@@ -241,15 +242,16 @@ Envs& norm_envs(tn_state* st, Layout& L, int R) {
       s.mats.push_back(L.A[v]);
       s.out.push_back(has(L, v, 0));
     }
-    FitResult fr = fit(c, s, R, 2, b + 1, st->seed, st->nh, logd.as<double>(), false);
-    double lg = 0;
-    TN_CUDA(cudaMemcpyAsync(&lg, logd.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    TN_CUDA(cudaStreamSynchronize(c.stream));
-    if (!std::isfinite(lg)) throw Error(TN_E_NUMERIC, "non-finite norm environment at row " + std::to_string(b + 1));
+    FitResult fr = fit(c, s, R, 2, b + 1, st->seed, st->nh, logd.as<double>() + (b - 1), false);
     E.M[b - 1] = fr.sites;
-    E.logs[b - 1] = lg;
   }
+  TN_CUDA(cudaMemcpyAsync(E.logs.data(), logd.p, sizeof(double) * nbr, cudaMemcpyDeviceToHost, c.stream));
   TN_CUDA(cudaStreamSynchronize(c.stream));
+  for (int b = 0; b + 1 < nbr; ++b)
+    if (!std::isfinite(E.logs[b])) {
+      L.envs.erase(R);
+      throw Error(TN_E_NUMERIC, "non-finite norm environment at row " + std::to_string(b + 2));
+    }
   E.ready = true;
   st->last_precompute_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return E;
@@ -555,8 +557,17 @@ int tn_load_state(const tn_graph* g, const double* const* tensors, int32_t chi, 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) throw Error(TN_E_CUDA, "no CUDA device");
     TN_CUDA(cudaGetDevice(&st->device));
+    {
+      // keep freed blocks in the stream-ordered pool across synchronisations (the default
+      // release threshold of 0 returns GBs of intermediates to the OS at every sync)
+      cudaMemPool_t pool;
+      TN_CUDA(cudaDeviceGetDefaultMemPool(&pool, st->device));
+      uint64_t thr = UINT64_MAX;
+      TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     TN_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
     st->ctx.stream = st->stream;
+    if (const char* gm = getenv("TN_GEMM")) st->ctx.gemm_mode = std::atoi(gm);  // debugging override
     *out = st.release();
   });
 }

@@ -39,3 +39,17 @@ if not a.skip_sample:
     dt = time.time() - t0
     print(f"sample n={a.n} {dt:.3f}s -> {a.n / dt:.1f} samples/s; stats {g.stats()}; flags {np.bincount(flags)}",
           flush=True)
+
+try:
+    import ctypes as C
+    from paper_2507_11424_b200 import _lib
+    LIB = _lib.lib()
+    ms = np.zeros(6)
+    cnt = np.zeros(6, dtype=np.int64)
+    on = LIB.tn_debug_profile(ms.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p), 6, 1)
+    if on:
+        names = ["gemm_tc", "gemm_simt", "permute", "orth", "tail", "misc"]
+        print("profile (ms, count, all calls in this process):",
+              {n: (round(m, 1), int(k)) for n, m, k in zip(names, ms, cnt)})
+except Exception as e:  # noqa
+    print("no profile:", e)

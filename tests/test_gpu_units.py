@@ -26,7 +26,7 @@ def dcontract(A, la, B, lb, lout, nb=1, perA=False, perB=False, cA=False, cB=Fal
     shB = B.shape[1:] if perB else B.shape
     A = np.ascontiguousarray(A, dtype=np.complex64)
     B = np.ascontiguousarray(B, dtype=np.complex64)
-    ref = np.einsum(f"{'Z' if perA else ''}{la},{'Z' if perB else ''}{lb}->{'Z' if (perA or perB) else ''}{lout}",
+    ref = np.einsum(f"{'Q' if perA else ''}{la},{'Q' if perB else ''}{lb}->{'Q' if (perA or perB) else ''}{lout}",
                     A.conj() if cA else A, B.conj() if cB else B)
     out = np.zeros(ref.shape, dtype=np.complex64)
     sa = (C.c_int * len(shA))(*shA)
@@ -82,6 +82,28 @@ def test_contract_batched_and_conj(gemm):
     A3 = rand(rng, (nb, 2, 3, 1, 4))
     B3 = rand(rng, (nb, 5, 2, 1, 4))
     out, ref = dcontract(A3, "saez", B3, "Asuz", "saeA", nb=nb, perA=True, perB=True, cB=True, gemm=gemm)
+    assert close(out, ref)
+
+
+@pytest.mark.parametrize("gemm", [1, 2])
+def test_contract_gather_views(gemm):
+    """Operands whose M/K axes are interleaved (the tensor-core path gathers them)."""
+    rng = np.random.default_rng(11)
+    nb = 3
+    A = rand(rng, (nb, 5, 6, 7))
+    B = rand(rng, (5, 7, 8))
+    out, ref = dcontract(A, "mxy", B, "myn", "xn", nb=nb, perA=True, gemm=gemm)
+    assert close(out, ref)
+    B2 = rand(rng, (nb, 5, 7, 8))
+    out, ref = dcontract(A, "mxy", B2, "myn", "xn", nb=nb, perA=True, perB=True, cB=True, gemm=gemm)
+    assert close(out, ref)
+    Y2 = rand(rng, (nb, 3, 2, 4, 5, 6))
+    N = rand(rng, (nb, 7, 2, 6, 4))
+    out, ref = dcontract(Y2, "asZeD", N, "AsDZ", "saeA", nb=nb, perA=True, perB=True, cB=True, gemm=gemm)
+    assert close(out, ref)
+    X1 = rand(rng, (4, 3, 2, 5, 6, 7))
+    Aop = rand(rng, (2, 9, 5, 3, 8))
+    out, ref = dcontract(X1, "xabdDf", Aop, "sudar", "xbDfsur", gemm=gemm)
     assert close(out, ref)
 
 
