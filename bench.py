@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""bench.py -- bitstring samples/s of generalised boundary-MPS sampling on B200 (BASELINE.json).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload NAME]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step = one pass of the whole per-sample hot path (row fit, right
+ladder, left pass + draw, project/merge, over every row) for one batch of samples per GPU,
+inputs (state, norm environments, uniforms) resident in HBM. The norm-environment
+precompute (a1) runs once before timing and is reported separately, as in the paper
+("following a pre-computed contraction of the norm network").
+Multi-GPU: weak scaling, samples sharded by rank; the state is NCCL-broadcast from rank 0,
+every rank recomputes the (deterministic) environments; no collective in the timed region.
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "bitstring samples/sec at 1/2/4/8 B200 (Willow-105, χ_env=128); TC-pipe util"
+
+# name: lattice, chi, chi_env, samples per GPU per step
+WORKLOADS = {
+    # the metric configuration: Willow-105 shapes of config 4 (chi = 32, chi_env = 128)
+    "willow105_chi32_env128": ("willow105", 32, 128, 2),
+    # parity / smaller shapes (not the metric)
+    "willow105_chi16_env64": ("willow105", 16, 64, 16),
+    "willow105_chi8_env32": ("willow105", 8, 32, 256),
+    "eagle127_chi16_env64": ("eagle127", 16, 64, 64),
+    "square6x6_chi8_env32": ("square6x6", 8, 32, 512),
+}
+DEFAULT_WORKLOAD = "willow105_chi32_env128"
+STATE_SEED = 2507
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampled during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[0]) for r in rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def make_state(lat, chi):
+    from tninputs import synthetic as S
+    return S.vidal_like(lat, chi, seed=STATE_SEED)
+
+
+def broadcast_state(st, lat, chi, rank, dist, torch, dev):
+    """NCCL broadcast of the TNS tensors from rank 0."""
+    from tninputs import synthetic as S
+    if rank == 0:
+        flat = np.concatenate([t.reshape(-1).view(np.float64) for t in st["tensors"]])
+        buf = torch.from_numpy(flat).to(dev)
+    else:
+        sizes = []
+        inc = S.incident_edges(lat.n, lat.edges)
+        for v in range(lat.n):
+            sizes.append(2 * 2 * chi ** len(inc[v]))
+        buf = torch.empty(sum(sizes), dtype=torch.float64, device=dev)
+    dist.broadcast(buf, 0)
+    if rank != 0:
+        host = buf.cpu().numpy()
+        tensors, off = [], 0
+        inc = S.incident_edges(lat.n, lat.edges)
+        for v in range(lat.n):
+            shape = (2,) + (chi,) * len(inc[v])
+            n = int(np.prod(shape))
+            tensors.append(host[off: off + 2 * n].view(np.complex128).reshape(shape).copy())
+            off += 2 * n
+        st = S.make_state(lat, tensors, [chi] * lat.n_edges, chi, {"kind": "vidal_like", "seed": STATE_SEED})
+    return st
+
+
+class LazyRandomM:
+    """Norm-environment sites with the shapes the method produces (R6), random values: the
+    oracle's sampling time does not depend on the values, and its own precompute at the
+    metric configuration would take days (SURVEY 0 finding 5)."""
+
+    def __init__(self, P, R, rng):
+        from oracle import bmps as B
+        self.B = B
+        self.P = P
+        self.R = R
+        self.rng = rng
+        nb = len(P.rows)
+        # shapes from the bottom row up, exactly as norm_envs() would produce them
+        self.shapes = [None] * nb
+        tops = None
+        for b in range(nb - 1, 0, -1):
+            row = P.rows[b]
+            fake = None if tops is None else [np.zeros(s, dtype=np.complex64) for s in tops]
+            tps = B._tops_for_row(P, row, fake, "down", "double")
+            strip = B.Strip("double", tps, [P.A[v] for v in row], [P.has(v, "up") for v in row])
+            D = B.bond_dims(strip, R)
+            cols = [j for j in range(len(row)) if P.has(row[j], "up")]
+            shp = [(D[k], P.A[row[c]].shape[1], P.A[row[c]].shape[1], D[k + 1]) for k, c in enumerate(cols)]
+            self.shapes[b - 1] = shp
+            tops = shp
+        self.cache = {}
+
+    def __getitem__(self, b):
+        if self.shapes[b] is None:
+            return None
+        if b not in self.cache:
+            self.cache = {}
+            sites = []
+            for s in self.shapes[b]:
+                x = (self.rng.standard_normal(s) + 1j * self.rng.standard_normal(s)) / math.sqrt(np.prod(s[1:]))
+                sites.append(x)
+            self.cache[b] = sites
+        return self.cache[b]
+
+
+def oracle_rate(st, lat, R, row_cmacs, budget_s, seed=7):
+    """Bounded timing of the CPU oracle (oracle/bmps.sample, as it stands) on the same
+    workload: rows are sampled in order until the budget is spent; samples/s is scaled by
+    the fraction of one sample's algorithmic complex MACs those rows carry."""
+    from oracle import bmps as B
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
+    except Exception:
+        threads = os.cpu_count()
+    t0 = time.time()
+    P = B.Prepared(st, lat.rows)
+    M = LazyRandomM(P, R, np.random.default_rng(seed))
+    setup = time.time() - t0
+    u = np.random.default_rng(seed).random(lat.n)
+    total = float(sum(row_cmacs)) if row_cmacs else 0.0
+    elapsed, rows_done = 0.0, 0
+    t0 = time.time()
+    for r in range(1, len(lat.rows) + 1):
+        B.sample(P, M, R, u, max_rows=r)
+        elapsed = time.time() - t0
+        rows_done = r
+        if elapsed >= budget_s:
+            break
+    # the loop re-runs rows 0..r-1 each time; charge the last run only
+    t1 = time.time()
+    B.sample(P, M, R, u, max_rows=rows_done)
+    last = time.time() - t1
+    frac = (sum(row_cmacs[:rows_done]) / total) if total > 0 else 1.0
+    rate = frac / last if last > 0 else float("nan")
+    return {"value": rate, "unit": "samples/s", "cores": int(threads), "kind": "oracle",
+            "sample": (f"one sample's first {rows_done}/{len(lat.rows)} rows ({100 * frac:.3g}% of its "
+                       f"algorithmic complex MACs) took {last:.1f} s on the host; samples/s scaled by that "
+                       f"fraction; random norm-environment sites of the method's shapes (oracle precompute "
+                       f"at this size takes days); setup {setup:.0f} s not timed")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0, help="samples per GPU per step (0 = workload default)")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    assert a.warmup >= 1 and a.steps >= 1
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    lat_name, chi, R, batch = WORKLOADS[a.workload]
+    if a.batch:
+        batch = a.batch
+    from tninputs import lattices as L
+    lat = L.by_name(lat_name)
+    config = {"workload": a.workload, "lattice": lat_name, "n_qubits": lat.n, "chi": chi, "chi_env": R,
+              "samples_per_gpu_per_step": batch, "fit_half_sweeps": 2, "row_order": "lattice rows",
+              "state": "synthetic Vidal-gauge-like TNS (dense, singular-value-weighted bonds, every bond at chi)",
+              "l2": "L2 flushed between timed steps (256 MB write); per-step working set >> 126 MB"}
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        st = make_state(lat, chi)
+        # rows' algorithmic cost shares from the cost model of the method (complex MACs per row)
+        shares = row_shares_model(st, lat, R)
+        vals = []
+        for i in range(a.warmup + a.steps):
+            cb = oracle_rate(st, lat, R, shares, budget_s=a.cpu_budget / 2)
+            if i >= a.warmup:
+                vals.append(cb["value"])
+        v = float(np.mean(vals))
+        out = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": a.gpus, "steps": a.steps,
+               "warmup": a.warmup, "ms_per_step": 1000.0 / v if v > 0 else None, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+               "config": config, "impl": "reference",
+               "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cb["cores"], "kind": "oracle",
+                                "sample": cb["sample"]},
+               "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    from paper_2507_11424_b200 import TNState, _lib
+    LIB = _lib.lib()
+    LIB.tn_debug_counters.argtypes = [C.c_void_p, C.c_int]
+    LIB.tn_debug_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+    LIB.tn_debug_set_profile.argtypes = [C.c_int]
+    LIB.tn_debug_row_cmacs.argtypes = [C.c_void_p, C.c_int]
+
+    t0 = time.time()
+    st = make_state(lat, chi) if rank == 0 else None
+    if world > 1:
+        st = broadcast_state(st, lat, chi, rank, dist, torch, dev)
+    g = TNState(st)
+    t_load = time.time() - t0
+    t0 = time.time()
+    g.prepare(lat.rows, R)
+    torch.cuda.synchronize()
+    t_pre = time.time() - t0
+    log(f"[rank {rank}] state {t_load:.1f}s, precompute {t_pre:.1f}s")
+
+    N = lat.n
+    nsteps = a.warmup + a.steps
+    # uniforms for the global sample indices of this rank (weak scaling: rank r owns batch r)
+    rng = np.random.default_rng(1005)
+    u_all = rng.random((nsteps * world * batch, N))
+    u_mine = np.stack([u_all[(s * world + rank) * batch:(s * world + rank + 1) * batch] for s in range(nsteps)])
+    u_dev = torch.from_numpy(u_mine).to(dev)
+    bits_dev = torch.empty((nsteps, batch, N), dtype=torch.uint8, device=dev)
+    logp_dev = torch.empty((nsteps, batch), dtype=torch.float64, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(s):
+        g.sample_dev(lat.rows, R, batch, u_dev[s].data_ptr(), bits_dev[s].data_ptr(), logp_dev[s].data_ptr(),
+                     0, 0, stream.cuda_stream)
+
+    for s in range(a.warmup):
+        step(s)
+        flush.zero_()
+    torch.cuda.synchronize()
+    cnt0 = np.zeros(4)
+    LIB.tn_debug_counters(cnt0.ctypes.data, 1)
+    prof = np.zeros(7)
+    LIB.tn_debug_set_profile(1)
+    LIB.tn_debug_profile(prof.ctypes.data, None, 7, 1)
+    clocks = Clocks(local)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(a.warmup, nsteps):
+        step(s)
+        flush.zero_()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    LIB.tn_debug_profile(prof.ctypes.data, None, 7, 1)
+    LIB.tn_debug_set_profile(0)
+    cnt = np.zeros(4)
+    LIB.tn_debug_counters(cnt.ctypes.data, 0)
+    rows = np.zeros(len(lat.rows))
+    LIB.tn_debug_row_cmacs(rows.ctypes.data, len(rows))
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * batch * a.steps / (ms / 1000.0)
+
+    # e2e through the public host API: H2D of the uniforms and D2H of bits + ln q inside
+    e2e_steps = 1 if chi >= 32 else a.steps
+    u_host = u_mine[a.warmup: a.warmup + e2e_steps]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(e2e_steps):
+        g.sample(lat.rows, R, u_host[s])
+    torch.cuda.synchronize()
+    te = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([te], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        te = float(t.item())
+    e2e = {"value": world * batch * e2e_steps / te, "unit": "samples/s",
+           "h2d_bytes_per_step": int(batch * N * 8), "d2h_bytes_per_step": int(batch * N * 1 + batch * 8 * 2),
+           "steps": e2e_steps}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    pk, which = peaks()
+    ratio = 1.1 / 2.25  # nominal dense TF32 / BF16
+    tf32_peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * ratio
+    tc_ms = prof[6]
+    tc_cmacs = cnt[1]
+    achieved = (8.0 * tc_cmacs) / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "tc_gemm_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(a.workload)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "tc_gemm_kernel (tcgen05 kind::tf32, TF32x3 complex GEMM)",
+                "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": (achieved / tf32_peak) if achieved else None, "traffic": traffic,
+                "peak_source": f"{which}: bf16_tflops_sustained x 1.1/2.25 (dense TF32/BF16 nominal ratio)",
+                "algorithmic": "8 real flops per complex MAC of the GEMM (M*N*K), counted once; the TF32x3 "
+                               "split issues 3x4 real MMAs per complex MAC, so frac <= 1/3 by construction",
+                "tc_launches": int(cnt[2]), "tc_ms_total": tc_ms, "tc_share_of_step": tc_ms / ms if ms else None,
+                "cmacs_per_sample": float(cnt[0]) / (batch * a.steps)}
+    out = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "c64", "data": "synthetic", "config": dict(config, precompute_s=t_pre),
+           "roofline": roofline, "e2e": e2e, "gpu_launches": int(cnt[3] - cnt0[3]), "clocks": clk,
+           "phase_ms": {k: float(v) for k, v in zip(["gemm_tc_incl_prep", "gemm_simt", "permute", "orth", "tail",
+                                                      "misc", "tc_kernel"], prof)}}
+    if world == 1 and not a.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = oracle_rate(st, lat, R, list(rows), budget_s=a.cpu_budget)
+        except Exception as e:  # pragma: no cover
+            out["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "oracle",
+                                   "sample": f"failed: {e}"}
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def row_shares_model(st, lat, R):
+    """Per-row complex-MAC shares for the reference arm (no GPU): the leading terms of the
+    ladder (3 chi_d^2 D^4-type GEMMs) and the row fit, per vertex, from the R6 bonds."""
+    from oracle import bmps as B
+    P = B.Prepared(st, lat.rows)
+    shares = []
+    for b, row in enumerate(P.rows):
+        tot = 0.0
+        for v in row:
+            _, u, d, l, r = P.A[v].shape
+            D = min(R, 4 * max(u, d, l, r) ** 2)
+            tot += 3.0 * d * d * D ** 4 + 2.0 * D * D * (2 * d) * u * l * r  # ladder + row fit
+        shares.append(tot)
+    return shares
+
+
+if __name__ == "__main__":
+    main()

@@ -392,7 +392,7 @@ def _merge(P: Prepared, row, sites):
     return out
 
 
-def sample(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2, forced=None):
+def sample(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2, forced=None, max_rows=None):
     """O5 for one sample: returns (bits[N] uint8 by vertex id, ln q, cond[N], flags).
     With `forced` (bits by vertex id) the draw is replaced by the given bits, which
     evaluates q(x) of any x (used to enumerate the whole distribution in tests).
@@ -408,6 +408,8 @@ def sample(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2,
     flags = 0
     m_prev = None
     for b, row in enumerate(P.rows):
+        if max_rows is not None and b >= max_rows:  # partial run (bounded CPU timing only)
+            break
         strip = _n_strip(P, b, m_prev)
         nsites, _ = fit(strip, R, TAG_N, b + 1, seed, nh)
         W = len(row)

@@ -76,3 +76,25 @@ extern "C" int tn_debug_gemm_bench(int M, int N, int K, int nb, int mode, int re
     return -1;
   }
 }
+
+// Counters for bench.py: [0] complex MACs issued, [1] of which on tcgen05, [2] tcgen05 GEMM
+// kernel launches, [3] all kernel launches of this library.
+extern "C" int tn_debug_counters(double* out, int reset) {
+  out[0] = tn::g_cmacs;
+  out[1] = tn::g_cmacs_tc;
+  out[2] = (double)tn::g_tc_launches;
+  out[3] = (double)tn::g_launches;
+  if (reset) {
+    tn::g_cmacs = 0;
+    tn::g_cmacs_tc = 0;
+    tn::g_tc_launches = 0;
+  }
+  return 0;
+}
+
+// Per-row complex MACs of the last sampled batch (all samples of the batch).
+extern "C" int tn_debug_row_cmacs(double* out, int n) {
+  int m = (int)tn::g_row_cmacs.size();
+  for (int i = 0; i < n && i < m; ++i) out[i] = tn::g_row_cmacs[i];
+  return m;
+}

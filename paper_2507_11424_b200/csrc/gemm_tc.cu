@@ -436,6 +436,7 @@ bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per
 
 bool gemm_tc(Ctx& c, const GemmDesc& g) {
   if (!tc_eligible(c, g.M, g.N, g.K, g.work_per_sample)) return false;
+  g_cmacs_tc += (double)g.M * g.N * g.K * g.nb1 * g.nb2;
   static bool attr = false;
   if (!attr) {
     TN_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
@@ -521,10 +522,9 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.sc2 = g.sc2;
     p.z0 = z0;
     p.accumulate = g.accumulate ? 1 : 0;
-    if (b_batched && z0 != 0) {
-      // B planes are indexed by the absolute z; the maps cover all nbz elements
-    }
     dim3 grid(Nrp / TC_BN, Mp / TC_BM, nz);
+    ProfScope ps(P_TC_KERNEL, c.stream);
+    ++g_tc_launches;
     if (b_batched) {
       // shift B coordinates by z0: rebuild maps at the chunk's base
       CUtensorMap mbh2 = make_map(bh.as<float>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);

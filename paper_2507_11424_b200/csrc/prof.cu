@@ -43,6 +43,12 @@ void Prof::flush() {
 
 }  // namespace tn
 
+extern "C" int tn_debug_set_profile(int on) {
+  tn::g_prof.flush();
+  tn::g_prof.on = on != 0;
+  return 0;
+}
+
 extern "C" int tn_debug_profile(double* out_ms, long* out_count, int n, int reset) {
   tn::g_prof.flush();
   for (int i = 0; i < n && i < tn::P_NCAT; ++i) {

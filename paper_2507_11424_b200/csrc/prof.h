@@ -7,7 +7,8 @@
 
 namespace tn {
 
-enum ProfCat { P_GEMM_TC = 0, P_GEMM_SIMT, P_PERMUTE, P_ORTH, P_TAIL, P_MISC, P_NCAT };
+// P_TC_KERNEL (the tcgen05 GEMM kernel alone) nests inside P_GEMM_TC (operand prep + kernel).
+enum ProfCat { P_GEMM_TC = 0, P_GEMM_SIMT, P_PERMUTE, P_ORTH, P_TAIL, P_MISC, P_TC_KERNEL, P_NCAT };
 
 struct Prof {
   bool on = false;

@@ -10,6 +10,9 @@ namespace tn {
 
 int64_t g_launches = 0;
 double g_cmacs = 0.0;
+double g_cmacs_tc = 0.0;
+int64_t g_tc_launches = 0;
+std::vector<double> g_row_cmacs;
 
 // tcgen05 path (gemm_tc.cu); returns false when the shape/layout is not eligible.
 bool gemm_tc(Ctx& c, const GemmDesc& g);

@@ -78,5 +78,8 @@ bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per
 
 // Flop accounting of the GEMMs issued (complex MACs), for the roofline report.
 extern double g_cmacs;
+extern double g_cmacs_tc;      // the part issued to the tcgen05 kernel
+extern int64_t g_tc_launches;  // tcgen05 GEMM kernel launches
+extern std::vector<double> g_row_cmacs;  // per-row complex MACs of the last sampled batch
 
 }  // namespace tn

@@ -291,7 +291,14 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
   DevBuf xbuf(sizeof(int) * nb, c.stream);
   std::vector<Tensor> m_prev;
   bool have_prev = false;
+  g_row_cmacs.assign(L.rows.size(), 0.0);
   for (int b = 0; b < (int)L.rows.size(); ++b) {
+    const double cm0 = g_cmacs;
+    struct RowCount {
+      int b;
+      double c0;
+      ~RowCount() { g_row_cmacs[b] = g_cmacs - c0; }
+    } row_count{b, cm0};
     const auto& row = L.rows[b];
     int W = (int)row.size();
     // a2: n_b = Fit_R(m_{b-1} psi_b), (s, d) open at every vertex
