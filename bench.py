@@ -106,6 +106,13 @@ class Clocks:
                 "samples": len(rows)}
 
 
+def shard_uniforms(u_all, nsteps, world, rank, batch):
+    """Rows of the global uniform matrix owned by `rank`: step s, rank r -> global samples
+    [(s*world + r)*batch, (s*world + r + 1)*batch) (weak scaling; SURVEY 8(b) determinism:
+    sample k always reads uniforms[k], whatever the GPU count)."""
+    return np.stack([u_all[(s * world + rank) * batch:(s * world + rank + 1) * batch] for s in range(nsteps)])
+
+
 def make_state(lat, chi):
     from tninputs import synthetic as S
     return S.vidal_like(lat, chi, seed=STATE_SEED)
@@ -293,7 +300,7 @@ def main():
     # uniforms for the global sample indices of this rank (weak scaling: rank r owns batch r)
     rng = np.random.default_rng(1005)
     u_all = rng.random((nsteps * world * batch, N))
-    u_mine = np.stack([u_all[(s * world + rank) * batch:(s * world + rank + 1) * batch] for s in range(nsteps)])
+    u_mine = shard_uniforms(u_all, nsteps, world, rank, batch)
     u_dev = torch.from_numpy(u_mine).to(dev)
     bits_dev = torch.empty((nsteps, batch, N), dtype=torch.uint8, device=dev)
     logp_dev = torch.empty((nsteps, batch), dtype=torch.float64, device=dev)

@@ -237,10 +237,32 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
   for (int j = 0; j < s.W; ++j)
     if (s.out[j]) cols.push_back(j);
   int K = (int)cols.size();
+  // Environments are rescaled to unit norm after every absorbed column (any positive rescale
+  // is allowed, R13); their accumulated ln-scales (per sample) keep the returned log-norms
+  // exact. This keeps long double-layer rows inside the FP32 range.
+  struct Env {
+    Tensor t;
+    std::shared_ptr<DevBuf> lg;  // double[nb]
+  };
+  auto fresh_log = [&]() {
+    auto p = std::make_shared<DevBuf>(sizeof(double) * nb, c.stream);
+    TN_CUDA(cudaMemsetAsync(p->p, 0, sizeof(double) * nb, c.stream));
+    return p;
+  };
+  auto rescaled = [&](Tensor t, const Env& parent) {
+    Env e;
+    e.t = t;
+    e.lg = std::make_shared<DevBuf>(sizeof(double) * nb, c.stream);
+    TN_CUDA(cudaMemcpyAsync(e.lg->p, parent.lg->p, sizeof(double) * nb, cudaMemcpyDeviceToDevice, c.stream));
+    normalize(c, e.t, nb, e.lg->as<double>(), true);
+    return e;
+  };
+  auto trivial_env = [&]() { return Env{ops.trivial(), fresh_log()}; };
   if (K == 0) {
-    Tensor L = ops.trivial();
-    for (int j = 0; j < s.W; ++j) L = ops.absorb_left(L, j, nullptr);
-    res.scalar = L;
+    Env L = trivial_env();
+    for (int j = 0; j < s.W; ++j) L = rescaled(ops.absorb_left(L.t, j, nullptr), L);
+    res.scalar = L.t;
+    res.scalar_log = L.lg;
     return res;
   }
   std::vector<int> D = fit_bonds(s, R);
@@ -262,34 +284,38 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
     Tensor np = contract(c, pv, "aq", false, C, "bq", true, "ab");
     o[k - 1] = view(np, prev.shape);
   }
-  auto env_left = [&](const Tensor& Lk, int k) {
-    Tensor L = ops.absorb_left(Lk, cols[k], &o[k]);
+  auto env_left = [&](const Env& Lk, int k) {
+    Env L = rescaled(ops.absorb_left(Lk.t, cols[k], &o[k]), Lk);
     int end = (k + 1 < K) ? cols[k + 1] : s.W;
-    for (int j = cols[k] + 1; j < end; ++j) L = ops.absorb_left(L, j, nullptr);
+    for (int j = cols[k] + 1; j < end; ++j) L = rescaled(ops.absorb_left(L.t, j, nullptr), L);
     return L;
   };
-  auto env_right = [&](const Tensor& Fk, int k) {
-    Tensor F = ops.absorb_right(Fk, cols[k], &o[k]);
+  auto env_right = [&](const Env& Fk, int k) {
+    Env F = rescaled(ops.absorb_right(Fk.t, cols[k], &o[k]), Fk);
     int start = (k >= 1) ? cols[k - 1] : -1;
-    for (int j = cols[k] - 1; j > start; --j) F = ops.absorb_right(F, j, nullptr);
+    for (int j = cols[k] - 1; j > start; --j) F = rescaled(ops.absorb_right(F.t, j, nullptr), F);
     return F;
   };
-  std::vector<Tensor> Lk(K), Fk(K);
+  std::vector<Env> Lk(K), Fk(K);
   {
-    Tensor L = ops.trivial();
-    for (int j = 0; j < cols[0]; ++j) L = ops.absorb_left(L, j, nullptr);
+    Env L = trivial_env();
+    for (int j = 0; j < cols[0]; ++j) L = rescaled(ops.absorb_left(L.t, j, nullptr), L);
     Lk[0] = L;
-    Tensor F = ops.trivial();
-    for (int j = s.W - 1; j > cols[K - 1]; --j) F = ops.absorb_right(F, j, nullptr);
+    Env F = trivial_env();
+    for (int j = s.W - 1; j > cols[K - 1]; --j) F = rescaled(ops.absorb_right(F.t, j, nullptr), F);
     Fk[K - 1] = F;
   }
   for (int k = K - 1; k >= 1; --k) Fk[k - 1] = env_right(Fk[k], k);
+  // environments the current centre was computed with (for its true scale)
+  Env cl = Lk[0], cf = Fk[0];
   for (int h = 0; h < nh; ++h) {
     if (h % 2 == 0) {
       for (int k = 0; k < K; ++k) {
         if (!(h > 0 && k == 0)) {
-          Tensor d = ops.derivative(Lk[k], cols[k], Fk[k]);
+          Tensor d = ops.derivative(Lk[k].t, cols[k], Fk[k].t);
           o[k] = view(d, o[k].shape);
+          cl = Lk[k];
+          cf = Fk[k];
         }
         if (k < K - 1) {
           o[k] = left_orth(c, o[k], nb);
@@ -299,8 +325,10 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
     } else {
       for (int k = K - 1; k >= 0; --k) {
         if (k != K - 1) {
-          Tensor d = ops.derivative(Lk[k], cols[k], Fk[k]);
+          Tensor d = ops.derivative(Lk[k].t, cols[k], Fk[k].t);
           o[k] = view(d, o[k].shape);
+          cl = Lk[k];
+          cf = Fk[k];
         }
         if (k > 0) {
           o[k] = right_orth(c, o[k], nb, nullptr);
@@ -310,7 +338,9 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
     }
   }
   int centre = (nh % 2 == 1) ? K - 1 : 0;
-  normalize(c, o[centre], nb, logn, accumulate);
+  DevBuf lc(sizeof(double) * nb, c.stream);
+  normalize(c, o[centre], nb, lc.as<double>(), false);
+  if (logn) log_add(c, logn, lc.as<double>(), cl.lg->as<double>(), cf.lg->as<double>(), nb, accumulate);
   res.sites = std::move(o);
   return res;
 }

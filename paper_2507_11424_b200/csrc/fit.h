@@ -18,12 +18,13 @@ struct DStrip {
   std::vector<Tensor> mats;
   std::vector<bool> out;
   bool per_sample = true;  // environments / outputs carry the sample batch
-  int64_t chunk_elems = (int64_t)1 << 29;  // budget for double-layer intermediates
+  int64_t chunk_elems = (int64_t)1 << 30;  // budget (elements) for double-layer intermediates
 };
 
 struct FitResult {
   std::vector<Tensor> sites;  // output MPS (empty when the strip has no output column)
   Tensor scalar;              // [1] per sample: exact contraction when no output column
+  std::shared_ptr<DevBuf> scalar_log;  // double[nb]: the scalar's true value is scalar * exp(scalar_log)
 };
 
 // Output bonds D_0..D_K by SURVEY R6 (+ neighbour consistency), identical to the oracle.

@@ -15,7 +15,12 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <string>
 
 #include "tensor.h"
 
@@ -37,6 +42,10 @@ constexpr int TC_THREADS = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 epil
 struct TcParams {
   int M, N;          // complex extents (epilogue bounds)
   int kblocks;       // padded real K / TC_BK
+  int ksplit;        // K splits (grid.z = nz * ksplit); > 1 writes partials to ws
+  int kb_per_split;  // k-blocks per split (multiple of TC_KC)
+  float2* ws;        // [split][z][M][N] partial sums when ksplit > 1
+  int64_t ws_split;  // elements per split slice
   int b_batched;     // B planes carry the batch index
   float2* C;
   int64_t cm;
@@ -141,13 +150,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
-  const int nblk = blockIdx.x, mblk = blockIdx.y, z = blockIdx.z;
+  const int nblk = blockIdx.x, mblk = blockIdx.y;
+  const int z = blockIdx.z / p.ksplit, split = blockIdx.z - z * p.ksplit;
+  const int kb0 = split * p.kb_per_split;
+  const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
+  const int nkb = kb1 - kb0;
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       const int bz = p.b_batched ? z : 0;
-      for (int kb = 0; kb < p.kblocks; ++kb) {
-        const int s = kb % TC_STAGES;
-        const uint32_t ph = (kb / TC_STAGES) & 1;
+      for (int i = 0; i < nkb; ++i) {
+        const int kb = kb0 + i;
+        const int s = i % TC_STAGES;
+        const uint32_t ph = (i / TC_STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
@@ -163,15 +177,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // kind::tf32 instruction descriptor: D f32, A/B tf32, K-major both, N=256, M=128
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
-      for (int kb = 0; kb < p.kblocks; ++kb) {
-        const int c = kb / TC_KC, buf = c & 1, kin = kb - c * TC_KC;
+      for (int i = 0; i < nkb; ++i) {
+        const int c = i / TC_KC, buf = c & 1, kin = i - c * TC_KC;
         if (kin == 0) {  // chunk c accumulates into TMEM buffer c&1 once the epilogue drained it
           mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
         }
         const uint32_t dacc = tmem + (uint32_t)(buf * TC_BN);
-        const int s = kb % TC_STAGES;
-        const uint32_t ph = (kb / TC_STAGES) & 1;
+        const int s = i % TC_STAGES;
+        const uint32_t ph = (i / TC_STAGES) & 1;
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
@@ -185,7 +199,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mma_tf32(dacc, alo + adv, bhi + adv, idesc, 1u);
         }
         mma_commit(&empty[s]);
-        if (kin == TC_KC - 1 || kb == p.kblocks - 1) mma_commit(&acc_full[buf]);
+        if (kin == TC_KC - 1 || i == nkb - 1) mma_commit(&acc_full[buf]);
       }
     }
     __syncwarp();
@@ -200,7 +214,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float acc[128];
 #pragma unroll
     for (int i = 0; i < 128; ++i) acc[i] = 0.f;
-    const int nchunks = (p.kblocks + TC_KC - 1) / TC_KC;
+    const int nchunks = (nkb + TC_KC - 1) / TC_KC;
     for (int c = 0; c < nchunks; ++c) {
       const int buf = c & 1;
       mbar_wait(&acc_full[buf], (c >> 1) & 1);
@@ -222,7 +236,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
-    if (row < p.M) {
+    if (row < p.M && p.ksplit > 1) {  // partial sum of this K split -> workspace
+      float2* W = p.ws + split * p.ws_split + ((int64_t)z * p.M + row) * p.N;
+      const int n0 = (nblk * TC_BN + half * 128) >> 1;
+#pragma unroll
+      for (int q = 0; q < 64; ++q) {
+        const int n = n0 + q;
+        if (n < p.N) W[n] = make_float2(acc[2 * q], acc[2 * q + 1]);
+      }
+    } else if (row < p.M) {
       const int b1 = (p.z0 + z) / p.nb2, b2 = (p.z0 + z) - b1 * p.nb2;
       float2* Crow = p.C + b1 * p.sc1 + b2 * p.sc2 + (int64_t)row * p.cm;
       const int n0 = (nblk * TC_BN + half * 128) >> 1;
@@ -245,6 +267,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// Deterministic split-K reduction: C (+)= sum over splits in a fixed order.
+__global__ void splitk_reduce_kernel(const float2* __restrict__ ws, int ksplit, int64_t ws_split, int nz, int M,
+                                     int N, float2* C, int64_t cm, int nb2, int64_t sc1, int64_t sc2, int z0,
+                                     int accumulate) {
+  const int64_t per = (int64_t)M * N, tot = per * nz;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t zz = e / per, r = e - zz * per;
+    const int row = (int)(r / N), n = (int)(r - (int64_t)row * N);
+    float2 s = ws[e];
+    for (int k = 1; k < ksplit; ++k) {
+      const float2 v = ws[k * ws_split + e];
+      s.x += v.x;
+      s.y += v.y;
+    }
+    const int z = z0 + (int)zz;
+    const int b1 = z / nb2, b2 = z - b1 * nb2;
+    float2* cp = C + b1 * sc1 + b2 * sc2 + (int64_t)row * cm + n;
+    if (accumulate) {
+      const float2 o = *cp;
+      s.x += o.x;
+      s.y += o.y;
+    }
+    *cp = s;
   }
 }
 
@@ -426,6 +474,57 @@ inline int rup(int x, int m) { return (x + m - 1) / m * m; }
 // depends on per-sample shapes only, so results do not depend on the batch size.
 static const double kTcMinWork = 1 << 20;
 
+// TN_GEMM_LOG=1: per-shape device time of the tensor-core GEMMs (prep + kernel), printed by
+// tn_debug_gemm_log() -- instrumentation for tuning only.
+namespace {
+struct ShapeRec {
+  std::string key;
+  cudaEvent_t a, b, c;  // a: before prep, b: before kernel, c: after
+  double cm;
+};
+std::vector<ShapeRec> g_shape_pending;
+std::map<std::string, std::array<double, 4>> g_shape_tab;  // count, prep ms, kernel ms, cmacs
+bool shape_log_on() {
+  static int on = -1;
+  if (on < 0) on = getenv("TN_GEMM_LOG") ? 1 : 0;
+  return on == 1;
+}
+void shape_flush() {
+  for (auto& r : g_shape_pending) {
+    cudaEventSynchronize(r.c);
+    float t1 = 0, t2 = 0;
+    cudaEventElapsedTime(&t1, r.a, r.b);
+    cudaEventElapsedTime(&t2, r.b, r.c);
+    auto& e = g_shape_tab[r.key];
+    e[0] += 1;
+    e[1] += t1;
+    e[2] += t2;
+    e[3] += r.cm;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+    cudaEventDestroy(r.c);
+  }
+  g_shape_pending.clear();
+}
+}  // namespace
+
+}  // namespace tn
+
+extern "C" int tn_debug_gemm_log(void) {
+  tn::shape_flush();
+  std::vector<std::pair<double, std::string>> rows;
+  for (auto& kv : tn::g_shape_tab) rows.push_back({kv.second[1] + kv.second[2], kv.first});
+  std::sort(rows.rbegin(), rows.rend());
+  for (size_t i = 0; i < rows.size() && i < 40; ++i) {
+    auto& e = tn::g_shape_tab[rows[i].second];
+    fprintf(stderr, "%-60s n=%6.0f prep=%9.1f ms kern=%9.1f ms  %.1f TF alg\n", rows[i].second.c_str(), e[0], e[1],
+            e[2], e[2] > 0 ? 8.0 * e[3] / (e[2] * 1e-3) / 1e12 : 0.0);
+  }
+  return (int)rows.size();
+}
+
+namespace tn {
+
 bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per_sample) {
   if (c.gemm_mode == 1) return false;
   if (M <= 0 || N <= 0 || K <= 0) return false;
@@ -437,6 +536,31 @@ bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per
 bool gemm_tc(Ctx& c, const GemmDesc& g) {
   if (!tc_eligible(c, g.M, g.N, g.K, g.work_per_sample)) return false;
   g_cmacs_tc += (double)g.M * g.N * g.K * g.nb1 * g.nb2;
+  ShapeRec srec;
+  const bool slog = shape_log_on();
+  if (slog) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "M=%d N=%d K=%d nb1=%d nb2=%d views=%d%d", g.M, g.N, g.K, g.nb1, g.nb2,
+             g.vam.rank > 0 ? 1 : 0, g.vbk.rank > 0 ? 1 : 0);
+    srec.key = buf;
+    srec.cm = (double)g.M * g.N * g.K * g.nb1 * g.nb2;
+    cudaEventCreate(&srec.a);
+    cudaEventCreate(&srec.b);
+    cudaEventCreate(&srec.c);
+    cudaEventRecord(srec.a, c.stream);
+  }
+  struct SlogEnd {
+    bool on;
+    ShapeRec& r;
+    cudaStream_t s;
+    ~SlogEnd() {
+      if (on) {
+        cudaEventRecord(r.c, s);
+        g_shape_pending.push_back(r);
+        if (g_shape_pending.size() > 2000) shape_flush();
+      }
+    }
+  } slog_end{slog, srec, c.stream};
   static bool attr = false;
   if (!attr) {
     TN_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
@@ -481,10 +605,28 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
   }
   CUtensorMap mbh = make_map(bh.as<float>(), Krp, Nrp, nzb, TC_BN);
   CUtensorMap mbl = make_map(bl.as<float>(), Krp, Nrp, nzb, TC_BN);
+  // Split-K when one sample's output has too few tiles to fill the SMs (long-K, small-MN
+  // GEMMs such as the fit derivatives). Chosen from per-sample shapes only (bitwise-identical
+  // results for any batch size); splits are whole promotion chunks.
+  const int kblocks = Krp / TC_BK;
+  const int mps = g.m_per_sample > 0 ? g.m_per_sample : g.M;
+  const int64_t tiles_ps = (int64_t)((mps + TC_BM - 1) / TC_BM) * (Nrp / TC_BN) * g.nb2;
+  int ksplit = 1, kbps = kblocks;
+  if (tiles_ps < 148 && kblocks >= 2 * TC_KC) {
+    int want = (int)std::min<int64_t>(32, (2 * 148 + tiles_ps - 1) / tiles_ps);
+    int maxs = kblocks / TC_KC;
+    ksplit = std::max(1, std::min(want, maxs));
+    kbps = ((kblocks + ksplit - 1) / ksplit + TC_KC - 1) / TC_KC * TC_KC;
+    ksplit = (kblocks + kbps - 1) / kbps;
+  }
   // A planes, chunked over the batch to bound the workspace (<= ~2 GB per plane)
   const int64_t per_z = (int64_t)Mp * Krp;
-  const int zc = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)nbz, (int64_t)65535, (int64_t)(1ll << 29) / std::max<int64_t>(1, per_z)}));
+  const int zc = (int)std::max<int64_t>(
+      1, std::min<int64_t>({(int64_t)nbz, (int64_t)(65535 / ksplit), (int64_t)(1ll << 29) / std::max<int64_t>(1, per_z)}));
   DevBuf ah((size_t)zc * per_z * 4, c.stream), al((size_t)zc * per_z * 4, c.stream);
+  DevBuf ws;
+  const int64_t ws_split = (int64_t)zc * g.M * g.N;
+  if (ksplit > 1) ws.alloc((size_t)ksplit * ws_split * sizeof(float2), c.stream);
   for (int z0 = 0; z0 < nbz; z0 += zc) {
     const int nz = std::min(zc, nbz - z0);
     {
@@ -513,7 +655,11 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     TcParams p;
     p.M = g.M;
     p.N = g.N;
-    p.kblocks = Krp / TC_BK;
+    p.kblocks = kblocks;
+    p.ksplit = ksplit;
+    p.kb_per_split = kbps;
+    p.ws = ws.as<float2>();
+    p.ws_split = ws_split;
     p.b_batched = b_batched ? 1 : 0;
     p.C = g.C;
     p.cm = g.cm;
@@ -522,18 +668,28 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.sc2 = g.sc2;
     p.z0 = z0;
     p.accumulate = g.accumulate ? 1 : 0;
-    dim3 grid(Nrp / TC_BN, Mp / TC_BM, nz);
-    ProfScope ps(P_TC_KERNEL, c.stream);
-    ++g_tc_launches;
-    if (b_batched) {
-      // shift B coordinates by z0: rebuild maps at the chunk's base
-      CUtensorMap mbh2 = make_map(bh.as<float>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
-      CUtensorMap mbl2 = make_map(bl.as<float>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
-      tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mbh2, mbl2, p);
-    } else {
-      tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mbh, mbl, p);
+    dim3 grid(Nrp / TC_BN, Mp / TC_BM, nz * ksplit);
+    if (slog && z0 == 0) cudaEventRecord(srec.b, c.stream);
+    {
+      ProfScope ps(P_TC_KERNEL, c.stream);
+      ++g_tc_launches;
+      if (b_batched) {
+        // shift B coordinates by z0: rebuild maps at the chunk's base
+        CUtensorMap mbh2 = make_map(bh.as<float>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
+        CUtensorMap mbl2 = make_map(bl.as<float>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
+        tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mbh2, mbl2, p);
+      } else {
+        tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mbh, mbl, p);
+      }
+      TN_LAUNCHED();
     }
-    TN_LAUNCHED();
+    if (ksplit > 1) {
+      int64_t tot = (int64_t)nz * g.M * g.N;
+      unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16);
+      splitk_reduce_kernel<<<blocks, 256, 0, c.stream>>>(p.ws, ksplit, ws_split, nz, g.M, g.N, g.C, g.cm, g.nb2,
+                                                         g.sc1, g.sc2, z0, p.accumulate);
+      TN_LAUNCHED();
+    }
   }
   return true;
 }

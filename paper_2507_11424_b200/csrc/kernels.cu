@@ -188,6 +188,13 @@ __global__ void add_kernel(float2* __restrict__ dst, int64_t dbs, const float2* 
   }
 }
 
+__global__ void log_add_kernel(double* out, const double* a, const double* b, const double* c, int n, bool acc) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = a[i] + (b ? b[i] : 0.0) + (c ? c[i] : 0.0);
+  out[i] = acc ? out[i] + v : v;
+}
+
 unsigned grid_for(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
 }  // namespace
@@ -277,6 +284,11 @@ void add_into(Ctx& c, Tensor& dst, const Tensor& src, int nb) {
   int n = dst.bstride ? nb : 1;
   int64_t size = dst.size();
   add_kernel<<<grid_for(size * n), 256, 0, c.stream>>>(dst.p, dst.bstride, src.p, src.bstride, size, n);
+  TN_LAUNCHED();
+}
+
+void log_add(Ctx& c, double* out, const double* a, const double* b, const double* c2, int n, bool acc) {
+  log_add_kernel<<<ceil_div(n, 128), 128, 0, c.stream>>>(out, a, b, c2, n, acc);
   TN_LAUNCHED();
 }
 

@@ -42,6 +42,9 @@ void copy_rows(Ctx& c, const Tensor& src, Tensor& dst, int64_t x0, int nb);
 // dst += src (elementwise, same size)
 void add_into(Ctx& c, Tensor& dst, const Tensor& src, int nb);
 
+// out[i] = (acc ? out[i] : 0) + a[i] + (b ? b[i] : 0) + (c ? c[i] : 0), i < n (device arrays)
+void log_add(Ctx& c, double* out, const double* a, const double* b, const double* c2, int n, bool acc);
+
 // out[b] = per-sample scalar t[b][0] -> host (complex) helper
 void scalars_to_host(Ctx& c, const Tensor& t, int nb, std::vector<float2>& out);
 

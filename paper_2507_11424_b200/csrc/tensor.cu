@@ -617,6 +617,7 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
   g.sb1 = Yu->bstride;
   g.sc1 = C.bstride;
   g.work_per_sample = Msz * Nsz * Ksz * Lsz;
+  g.m_per_sample = (int)Msz;
   if (Ksz == 0 || Msz == 0 || Nsz == 0) { zero(c, C, g.nb1); }
   if (views) {
     g.vam = gv.vam;

@@ -71,6 +71,7 @@ struct GemmDesc {
   int64_t sa1 = 0, sb1 = 0, sc1 = 0, sa2 = 0, sb2 = 0, sc2 = 0;
   bool accumulate = false;
   int64_t work_per_sample = 0;  // complex MACs of one sample (kernel choice must not depend on batch)
+  int m_per_sample = 0;         // M before the sample batch was folded into it
 };
 void gemm(Ctx& c, const GemmDesc& g);
 // Whether gemm() will route a GEMM of this per-sample shape to the tensor cores.

@@ -405,12 +405,13 @@ void amplitude_batch(tn_state* st, Layout& L, int R, int nb, const uint8_t* bits
     if (fr.sites.empty()) {
       std::vector<float2> sc;
       scalars_to_host(c, fr.scalar, nb, sc);
-      std::vector<double> ln(nb);
+      std::vector<double> ln(nb), sl(nb);
       TN_CUDA(cudaMemcpyAsync(ln.data(), logn.p, sizeof(double) * nb, cudaMemcpyDeviceToHost, c.stream));
+      TN_CUDA(cudaMemcpyAsync(sl.data(), fr.scalar_log->p, sizeof(double) * nb, cudaMemcpyDeviceToHost, c.stream));
       TN_CUDA(cudaStreamSynchronize(c.stream));
       for (int k = 0; k < nb; ++k) {
         double a = std::hypot((double)sc[k].x, (double)sc[k].y);
-        logabs[k] = a > 0 ? ln[k] + std::log(a) : -INFINITY;
+        logabs[k] = a > 0 ? ln[k] + sl[k] + std::log(a) : -INFINITY;
         phase[k] = std::atan2((double)sc[k].y, (double)sc[k].x);
       }
       return;
@@ -710,7 +711,9 @@ int tn_log_norm(tn_state* st, int32_t chi_env, double* out_lognorm) {
     FitResult fr = fit(c, s, 1, 2, 1, st->seed, st->nh, nullptr, false);
     std::vector<float2> sc;
     scalars_to_host(c, fr.scalar, 1, sc);
-    double tot = 0;
+    double sl = 0;
+    TN_CUDA(cudaMemcpy(&sl, fr.scalar_log->p, sizeof(double), cudaMemcpyDeviceToHost));
+    double tot = sl;
     for (double x : E.logs) tot += x;
     *out_lognorm = std::log(std::hypot((double)sc[0].x, (double)sc[0].y)) + tot;
   });

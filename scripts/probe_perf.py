@@ -1,5 +1,6 @@
 """Timing probe: prepare (norm environments) + sampling on synthetic Vidal-like states."""
 import argparse
+import os
 import time
 
 import numpy as np
@@ -53,3 +54,5 @@ try:
               {n: (round(m, 1), int(k)) for n, m, k in zip(names, ms, cnt)})
 except Exception as e:  # noqa
     print("no profile:", e)
+if os.environ.get("TN_GEMM_LOG"):
+    LIB.tn_debug_gemm_log()

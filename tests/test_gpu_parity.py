@@ -113,6 +113,24 @@ def test_branch_superposition_full_topology(lat_name, chi, K, R):
             assert abs(a - b_) <= 1e-4 * b_ + (1e-6 if b_ < 1e-2 else 0), (k, got, ref)
 
 
+def test_branch_superposition_willow_full_chi():
+    """Full metric-config tensor shapes (Willow-105, every bond chi = 32, dense tensors) in the
+    exact regime: K = 4 branches -> boundary ranks <= 4 (single) / 16 (double) <= chi_env = 16,
+    so q(x) and every conditional have the closed form of the branch sum (maths, not the
+    oracle). Exercises the tcgen05 path at chi = 32 GEMM shapes."""
+    from tests.test_oracle import closed_form_conditionals
+    lat = L.willow105()
+    st = S.branch_superposition(lat, 32, 4, seed=11)
+    u = S.uniforms(4, lat.n, 12)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 16, u)
+    order = order_of(lat.rows)
+    for k in range(len(u)):
+        ref = closed_form_conditionals(st["meta"]["phis"], order, bits[k])
+        for v, r in zip(order, ref):
+            assert abs(cond[k, v] - r) <= 1e-4 * r + (1e-6 if r < 1e-2 else 0), (k, v, cond[k, v], r)
+        assert abs(logq[k] - sum(math.log(r) for r in ref)) <= 1e-4 * max(1, abs(logq[k]))
+
+
 def test_ghz_eagle():
     lat = L.eagle127()
     st = S.ghz(lat, chi=2)
