@@ -1,18 +1,27 @@
 // gemm_tc.cu -- complex GEMM on the 5th-generation tensor cores (tcgen05, sm_100a),
-// FP32-accurate through the TF32x3 split (K1 of SURVEY 2.4).
+// FP32-accurate through an FP16x3 split with exact power-of-two row/column scaling (K1 of
+// SURVEY 2.4).
 //
 // Complex C = A B is one real GEMM  C_r[M][2N] = A_r[M][2K] . B_r[2K][2N]:
 //   A_r = A viewed as interleaved (re, im) along K; C_r = C viewed the same way along N;
-//   B_r^T row 2n   = (Re b_kn, -Im b_kn) over k,  row 2n+1 = (Im b_kn, Re b_kn)  (K-major).
-// Every real operand x is split x = hi + lo with hi = x truncated to TF32 (exact split), and
-// D = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulates in FP32 in tensor memory (TMEM).
+//   B_r^T row 2n = (Re b_kn, -Im b_kn) over k, row 2n+1 = (Im b_kn, Re b_kn)  (K-major).
+// Each row m of A (each column n of B) is scaled by an exact power of two s so that its
+// largest |component| lies in [1/2, 1); every scaled value x is split into FP16 x = h + l
+// (h = fp16_rn(x), l = fp16_rn(x - h); 22 significant bits), and
+// D = A_h B_h + A_h B_l + A_l B_h accumulates in FP32; the epilogue multiplies by 1/(s_m s_n).
+// FP16 MMAs run at twice the TF32 rate and halve the operand bytes per K.
 //
-// Data flow: prep kernels write packed, zero-padded, K-major hi/lo planes to HBM; the GEMM
-// kernel streams 128x32 (A) and 256x32 (B) FP32 tiles with TMA (SWIZZLE_128B) through a
-// 2-stage mbarrier pipeline; one elected thread issues tcgen05.mma (M=128, N=256, K=8,
-// kind::tf32) into a 128x256 FP32 TMEM accumulator; four epilogue warps drain TMEM with
-// tcgen05.ld and write complex64 results.
+// Data flow: a max pass and a prep pass gather each operand straight from its multi-axis
+// layout (View4) into packed, zero-padded, K-major FP16 hi/lo planes in HBM; the GEMM kernel
+// streams 128x64 (A) and 256x64 (B) FP16 tiles with TMA (SWIZZLE_128B) through a 2-stage
+// mbarrier pipeline; one elected thread issues tcgen05.mma (M=128, N=256, K=16,
+// kind::f16, FP32 accumulate) into one of two 128x256 FP32 TMEM accumulators; every K chunk
+// of 1024 is promoted by eight epilogue warps into FP32 registers (the tensor core's FP32
+// accumulation truncates -- measured error grew linearly with K before chunking) while the
+// MMA fills the other accumulator. Long-K/small-MN GEMMs are split along K (deterministic
+// reduction).
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <array>
@@ -29,14 +38,15 @@ namespace {
 
 constexpr int TC_BM = 128;        // rows per CTA (UMMA M)
 constexpr int TC_BN = 256;        // real columns per CTA (UMMA N) = 128 complex columns
-constexpr int TC_BK = 32;         // real K per stage (one 128-byte swizzle atom of FP32)
+constexpr int TC_BK = 64;         // real K per stage (one 128-byte swizzle atom of FP16)
+constexpr int TC_UK = 16;         // K per kind::f16 MMA
 constexpr int TC_STAGES = 2;
-constexpr int A_TILE = TC_BM * TC_BK * 4;               // 16 KB
-constexpr int B_TILE = TC_BN * TC_BK * 4;               // 32 KB
+constexpr int A_TILE = TC_BM * TC_BK * 2;               // 16 KB
+constexpr int B_TILE = TC_BN * TC_BK * 2;               // 32 KB
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;    // 96 KB
 constexpr int SMEM_BYTES = TC_STAGES * STAGE_BYTES + 1024 + 256;
 constexpr uint32_t TMEM_COLS = 512;   // two 128x256 FP32 accumulators (ping-pong over K chunks)
-constexpr int TC_KC = 16;             // k-blocks (16 x 32 real K) per promoted chunk
+constexpr int TC_KC = 16;             // k-blocks (16 x 64 real K) per promoted chunk
 constexpr int TC_THREADS = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 
 struct TcParams {
@@ -47,6 +57,9 @@ struct TcParams {
   float2* ws;        // [split][z][M][N] partial sums when ksplit > 1
   int64_t ws_split;  // elements per split slice
   int b_batched;     // B planes carry the batch index
+  const float* amax; // [z][Mp] row maxima of A (scales)
+  const float* bmax; // [zb][Np] column maxima of B
+  int Mp, Np;
   float2* C;
   int64_t cm;
   int nb2;
@@ -94,25 +107,33 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
-  d |= (uint64_t)(0) << 16;                   // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(0) << 16;                     // LBO (unused for swizzled K-major)
   d |= (uint64_t)((1024 >> 4) & 0x3FFF) << 32;  // SBO
-  d |= (uint64_t)1 << 46;                     // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                     // SWIZZLE_128B
+  d |= (uint64_t)1 << 46;                       // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                       // SWIZZLE_128B
   return d;
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+
+// 1 / s for a row or column maximum mx (s = 2^-e, mx = f 2^e, f in [1/2, 1)).
+__device__ __forceinline__ float inv_scale(float mx) {
+  if (!(mx > 0.f)) return 1.f;
+  int e;
+  frexpf(mx, &e);
+  return ldexpf(1.f, e);
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -155,9 +176,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int kb0 = split * p.kb_per_split;
   const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
   const int nkb = kb1 - kb0;
+  const int bz = p.b_batched ? z : 0;
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      const int bz = p.b_batched ? z : 0;
       for (int i = 0; i < nkb; ++i) {
         const int kb = kb0 + i;
         const int s = i % TC_STAGES;
@@ -174,8 +195,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
-      // kind::tf32 instruction descriptor: D f32, A/B tf32, K-major both, N=256, M=128
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
+      // kind::f16 instruction descriptor: D f32, A/B f16, K-major both, N=256, M=128
+      const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
       for (int i = 0; i < nkb; ++i) {
         const int c = i / TC_KC, buf = c & 1, kin = i - c * TC_KC;
@@ -192,11 +213,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint64_t ahi = smem_desc(base), alo = smem_desc(base + A_TILE);
         const uint64_t bhi = smem_desc(base + 2 * A_TILE), blo = smem_desc(base + 2 * A_TILE + B_TILE);
 #pragma unroll
-        for (int k = 0; k < TC_BK / 8; ++k) {
-          const uint64_t adv = (uint64_t)((k * 32) >> 4);  // 8 tf32 = 32 bytes along K
-          mma_tf32(dacc, ahi + adv, bhi + adv, idesc, (kin | k) != 0);
-          mma_tf32(dacc, ahi + adv, blo + adv, idesc, 1u);
-          mma_tf32(dacc, alo + adv, bhi + adv, idesc, 1u);
+        for (int k = 0; k < TC_BK / TC_UK; ++k) {
+          const uint64_t adv = (uint64_t)((k * TC_UK * 2) >> 4);  // 16 halves = 32 bytes along K
+          mma_f16(dacc, ahi + adv, bhi + adv, idesc, (kin | k) != 0);
+          mma_f16(dacc, ahi + adv, blo + adv, idesc, 1u);
+          mma_f16(dacc, alo + adv, bhi + adv, idesc, 1u);
         }
         mma_commit(&empty[s]);
         if (kin == TC_KC - 1 || i == nkb - 1) mma_commit(&acc_full[buf]);
@@ -206,8 +227,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // epilogue: warps 2..9; warp w drains TMEM lanes 32*(w%4)..+31 (its rows) and columns
     // [128*h, 128*h + 128), h = (w-2)/4. Each K chunk's partial sum is promoted from TMEM
-    // into FP32 registers (round-to-nearest adds), which bounds the error of the tensor
-    // core's truncating accumulation to one chunk.
+    // into FP32 registers (round-to-nearest adds).
     const int lg = warp & 3;
     const int half = (warp - 2) >> 2;
     const int row = mblk * TC_BM + lg * 32 + lane;
@@ -236,29 +256,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
-    if (row < p.M && p.ksplit > 1) {  // partial sum of this K split -> workspace
-      float2* W = p.ws + split * p.ws_split + ((int64_t)z * p.M + row) * p.N;
+    if (row < p.M) {
+      const float rs = inv_scale(p.amax[(int64_t)z * p.Mp + row]);
+      const float* bmx = p.bmax + (int64_t)bz * p.Np;
       const int n0 = (nblk * TC_BN + half * 128) >> 1;
+      if (p.ksplit > 1) {  // partial sum of this K split -> workspace
+        float2* W = p.ws + split * p.ws_split + ((int64_t)z * p.M + row) * p.N;
 #pragma unroll
-      for (int q = 0; q < 64; ++q) {
-        const int n = n0 + q;
-        if (n < p.N) W[n] = make_float2(acc[2 * q], acc[2 * q + 1]);
-      }
-    } else if (row < p.M) {
-      const int b1 = (p.z0 + z) / p.nb2, b2 = (p.z0 + z) - b1 * p.nb2;
-      float2* Crow = p.C + b1 * p.sc1 + b2 * p.sc2 + (int64_t)row * p.cm;
-      const int n0 = (nblk * TC_BN + half * 128) >> 1;
-#pragma unroll
-      for (int q = 0; q < 64; ++q) {
-        const int n = n0 + q;
-        if (n < p.N) {
-          float2 val = make_float2(acc[2 * q], acc[2 * q + 1]);
-          if (p.accumulate) {
-            float2 o = Crow[n];
-            val.x += o.x;
-            val.y += o.y;
+        for (int q = 0; q < 64; ++q) {
+          const int n = n0 + q;
+          if (n < p.N) {
+            const float sc = rs * inv_scale(bmx[n]);
+            W[n] = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
           }
-          Crow[n] = val;
+        }
+      } else {
+        const int b1 = (p.z0 + z) / p.nb2, b2 = (p.z0 + z) - b1 * p.nb2;
+        float2* Crow = p.C + b1 * p.sc1 + b2 * p.sc2 + (int64_t)row * p.cm;
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          const int n = n0 + q;
+          if (n < p.N) {
+            const float sc = rs * inv_scale(bmx[n]);
+            float2 val = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
+            if (p.accumulate) {
+              float2 o = Crow[n];
+              val.x += o.x;
+              val.y += o.y;
+            }
+            Crow[n] = val;
+          }
         }
       }
     }
@@ -296,30 +323,6 @@ __global__ void splitk_reduce_kernel(const float2* __restrict__ ws, int ksplit, 
   }
 }
 
-__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
-
-// A_r hi/lo planes: [z][Mp][Krp], element (m, kr) = Re/Im of A(m, kr/2)
-__global__ void prep_a_kernel(const float2* __restrict__ A, int64_t am, int64_t ak, int conj, int nb2, int64_t sa1,
-                              int64_t sa2, int z0, int M, int K, int Mp, int Krp, float* __restrict__ hi,
-                              float* __restrict__ lo, int nz) {
-  const int64_t per = (int64_t)Mp * Krp, tot = per * nz;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t zz = e / per, r = e - zz * per;
-    const int m = (int)(r / Krp), kr = (int)(r - (int64_t)m * Krp);
-    const int k = kr >> 1;
-    float x = 0.f;
-    if (m < M && k < K) {
-      const int z = z0 + (int)zz;
-      const int b1 = z / nb2, b2 = z - b1 * nb2;
-      const float2 a = A[b1 * sa1 + b2 * sa2 + m * am + k * ak];
-      x = (kr & 1) ? (conj ? -a.y : a.y) : a.x;
-    }
-    const float h = tf32_trunc(x);
-    hi[e] = h;
-    lo[e] = x - h;
-  }
-}
-
 __device__ __forceinline__ int64_t view_off(const View4& v, int64_t idx) {
   int64_t off = 0;
 #pragma unroll
@@ -333,11 +336,9 @@ __device__ __forceinline__ int64_t view_off(const View4& v, int64_t idx) {
   return off;
 }
 
-// Tiled gather of an operand X(r, k) (r = row index M or N, k = K index; both compound,
-// View4) into TF32 hi/lo planes. 32 rows x 32 complex k per block through shared memory:
-// loads run along whichever side is contiguous in memory (k_fast), stores along the plane's
-// K axis. kind 0: A planes [z][Rp][Krp], element (r, 2k+c) = (Re, Im)[c];
-// kind 1: B_r^T planes [z][2*Rp'][Krp], rows 2r = (Re b, -Im b), 2r+1 = (Im b, Re b).
+// Operand X(r, k) (r = row index: M for A, N for B; k = K index; both compound, View4).
+// Tiles of 32 rows x 32 complex k through shared memory: loads run along whichever side is
+// contiguous in memory (k_fast), stores along the plane's K axis.
 struct PrepArgs {
   const float2* X;
   View4 vr, vk;
@@ -345,16 +346,14 @@ struct PrepArgs {
   int64_t s1, s2;
   int z0, R, K, Rrows, Krp;  // Rrows: padded plane rows (A: Mp; B: Nrp)
   int k_fast;
-  float* hi;
-  float* lo;
+  float* mx;                 // [z][Rp] row maxima (max pass writes, prep reads)
+  int Rp;                    // row count of mx per z (complex rows)
+  __half* hi;
+  __half* lo;
 };
 
-template <int KIND>
-__global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
-  __shared__ float2 tile[32][33];
-  __shared__ int64_t roff[32], koff[32];
-  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
-  const int zz = blockIdx.z;
+__device__ __forceinline__ void load_tile(const PrepArgs& a, float2 (*tile)[33], int64_t* roff, int64_t* koff,
+                                          int r0, int k0, int zz) {
   const int z = a.z0 + zz;
   const int b1 = z / a.nb2, b2 = z - b1 * a.nb2;
   const float2* base = a.X + b1 * a.s1 + b2 * a.s2;
@@ -371,23 +370,66 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
     tile[rr][kk] = v;
   }
   __syncthreads();
+}
+
+// Pass 1: max |component| of every row over K (atomicMax on the IEEE bits of a non-negative
+// float is order-independent, hence deterministic).
+__global__ void __launch_bounds__(256) rowmax_kernel(PrepArgs a) {
+  __shared__ float2 tile[32][33];
+  __shared__ int64_t roff[32], koff[32];
+  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32, zz = blockIdx.z;
+  load_tile(a, tile, roff, koff, r0, k0, zz);
+  const int t = threadIdx.x;
+  if (t < 32 && r0 + t < a.R) {
+    float m = 0.f;
+    for (int k = 0; k < 32; ++k) m = fmaxf(m, fmaxf(fabsf(tile[t][k].x), fabsf(tile[t][k].y)));
+    if (m > 0.f) atomicMax(reinterpret_cast<unsigned int*>(a.mx + (int64_t)zz * a.Rp + r0 + t), __float_as_uint(m));
+  }
+}
+
+__device__ __forceinline__ void split16(float x, __half& h, __half& l) {
+  h = __float2half_rn(x);
+  l = __float2half_rn(x - __half2float(h));
+}
+
+// Pass 2: scaled FP16 hi/lo planes. KIND 0: A planes [z][Rrows][Krp], element (r, 2k+c) =
+// (Re, Im)[c]. KIND 1: B_r^T planes [z][Rrows][Krp], rows 2r = (Re b, -Im b), 2r+1 = (Im b, Re b).
+template <int KIND>
+__global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
+  __shared__ float2 tile[32][33];
+  __shared__ int64_t roff[32], koff[32];
+  __shared__ float scl[32];
+  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32, zz = blockIdx.z;
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  if (t < 32) {
+    const float m = (r0 + t < a.R) ? a.mx[(int64_t)zz * a.Rp + r0 + t] : 0.f;
+    scl[t] = 1.f;
+    if (m > 0.f) {
+      int e;
+      frexpf(m, &e);
+      scl[t] = ldexpf(1.f, -e);
+    }
+  }
+  load_tile(a, tile, roff, koff, r0, k0, zz);
   const int64_t plane = (int64_t)a.Rrows * a.Krp;
   if (KIND == 0) {
     for (int j = ty; j < 32; j += 8) {
       const int r = r0 + j;
       if (r >= a.Rrows) continue;
-      float* hrow = a.hi + zz * plane + (int64_t)r * a.Krp;
-      float* lrow = a.lo + zz * plane + (int64_t)r * a.Krp;
+      __half* hrow = a.hi + zz * plane + (int64_t)r * a.Krp;
+      __half* lrow = a.lo + zz * plane + (int64_t)r * a.Krp;
+      const float s = scl[j];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int kr2 = tx + 32 * h;  // 0..63 real columns of this tile
         const int kr = 2 * k0 + kr2;
         if (kr >= a.Krp) continue;
         const float2 v = tile[j][kr2 >> 1];
-        const float x = (kr2 & 1) ? v.y : v.x;
-        const float hv = tf32_trunc(x);
+        const float x = ((kr2 & 1) ? v.y : v.x) * s;
+        __half hv, lv;
+        split16(x, hv, lv);
         hrow[kr] = hv;
-        lrow[kr] = x - hv;
+        lrow[kr] = lv;
       }
     }
   } else {
@@ -395,8 +437,9 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
       const int rr = j >> 1, par = j & 1;
       const int row = 2 * r0 + j;
       if (row >= a.Rrows) continue;
-      float* hrow = a.hi + zz * plane + (int64_t)row * a.Krp;
-      float* lrow = a.lo + zz * plane + (int64_t)row * a.Krp;
+      __half* hrow = a.hi + zz * plane + (int64_t)row * a.Krp;
+      __half* lrow = a.lo + zz * plane + (int64_t)row * a.Krp;
+      const float s = scl[rr];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int kr2 = tx + 32 * h;
@@ -404,36 +447,13 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
         if (kr >= a.Krp) continue;
         const float2 b = tile[rr][kr2 >> 1];
         const int sel = (par << 1) | (kr2 & 1);
-        const float x = sel == 0 ? b.x : (sel == 1 ? -b.y : (sel == 2 ? b.y : b.x));
-        const float hv = tf32_trunc(x);
+        const float x = (sel == 0 ? b.x : (sel == 1 ? -b.y : (sel == 2 ? b.y : b.x))) * s;
+        __half hv, lv;
+        split16(x, hv, lv);
         hrow[kr] = hv;
-        lrow[kr] = x - hv;
+        lrow[kr] = lv;
       }
     }
-  }
-}
-
-// B_r^T hi/lo planes: [z][Nrp][Krp]; row 2n = (Re b, -Im b), row 2n+1 = (Im b, Re b)
-__global__ void prep_b_kernel(const float2* __restrict__ B, int64_t bk, int64_t bn, int conj, int nb2, int64_t sb1,
-                              int64_t sb2, int z0, int N, int K, int Nrp, int Krp, float* __restrict__ hi,
-                              float* __restrict__ lo, int nz) {
-  const int64_t per = (int64_t)Nrp * Krp, tot = per * nz;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t zz = e / per, r = e - zz * per;
-    const int nr = (int)(r / Krp), kr = (int)(r - (int64_t)nr * Krp);
-    const int n = nr >> 1, k = kr >> 1;
-    float x = 0.f;
-    if (n < N && k < K) {
-      const int z = z0 + (int)zz;
-      const int b1 = z / nb2, b2 = z - b1 * nb2;
-      float2 b = B[b1 * sb1 + b2 * sb2 + k * bk + n * bn];
-      if (conj) b.y = -b.y;
-      const int sel = ((nr & 1) << 1) | (kr & 1);
-      x = sel == 0 ? b.x : (sel == 1 ? -b.y : (sel == 2 ? b.y : b.x));
-    }
-    const float h = tf32_trunc(x);
-    hi[e] = h;
-    lo[e] = x - h;
   }
 }
 
@@ -453,13 +473,13 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-CUtensorMap make_map(float* base, int inner, int rows, int nz, int box_rows) {
+CUtensorMap make_map(__half* base, int inner, int rows, int nz, int box_rows) {
   CUtensorMap m;
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)nz};
-  cuuint64_t strides[2] = {(cuuint64_t)inner * 4, (cuuint64_t)inner * rows * 4};
+  cuuint64_t strides[2] = {(cuuint64_t)inner * 2, (cuuint64_t)inner * rows * 2};
   cuuint32_t box[3] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, base, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(-5, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -468,15 +488,8 @@ CUtensorMap make_map(float* base, int inner, int rows, int nz, int box_rows) {
 
 inline int rup(int x, int m) { return (x + m - 1) / m * m; }
 
-}  // namespace
-
-// Per-sample work (complex MACs) above which the tensor-core path is used. The decision
-// depends on per-sample shapes only, so results do not depend on the batch size.
-static const double kTcMinWork = 1 << 20;
-
 // TN_GEMM_LOG=1: per-shape device time of the tensor-core GEMMs (prep + kernel), printed by
 // tn_debug_gemm_log() -- instrumentation for tuning only.
-namespace {
 struct ShapeRec {
   std::string key;
   cudaEvent_t a, b, c;  // a: before prep, b: before kernel, c: after
@@ -506,7 +519,12 @@ void shape_flush() {
   }
   g_shape_pending.clear();
 }
+
 }  // namespace
+
+// Per-sample work (complex MACs) above which the tensor-core path is used. The decision
+// depends on per-sample shapes only, so results do not depend on the batch size.
+static const double kTcMinWork = 1 << 20;
 
 }  // namespace tn
 
@@ -569,11 +587,9 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
   const int Krp = rup(2 * g.K, TC_BK);
   const int Mp = rup(g.M, TC_BM);
   const int Nrp = rup(2 * g.N, TC_BN);
+  const int Np = Nrp / 2;
   const int nbz = g.nb1 * g.nb2;
   const bool b_batched = (g.sb1 != 0 && g.nb1 > 1) || (g.sb2 != 0 && g.nb2 > 1);
-  // B planes (once, or per batch element)
-  const int nzb = b_batched ? nbz : 1;
-  DevBuf bh((size_t)nzb * Nrp * Krp * 4, c.stream), bl((size_t)nzb * Nrp * Krp * 4, c.stream);
   auto simple = [](int64_t dim, int64_t stride) {
     View4 v;
     v.rank = 1;
@@ -582,6 +598,11 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     return v;
   };
   auto inner_unit = [](const View4& v) { return v.rank > 0 && v.str[v.rank - 1] == 1; };
+  // ---- B planes (once, or per batch element)
+  const int nzb = b_batched ? nbz : 1;
+  DevBuf bh((size_t)nzb * Nrp * Krp * 2, c.stream), bl((size_t)nzb * Nrp * Krp * 2, c.stream);
+  DevBuf bmx((size_t)nzb * Np * sizeof(float), c.stream);
+  TN_CUDA(cudaMemsetAsync(bmx.p, 0, (size_t)nzb * Np * sizeof(float), c.stream));
   {
     PrepArgs a;
     a.X = g.B;
@@ -597,17 +618,22 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     a.Rrows = Nrp;
     a.Krp = Krp;
     a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
-    a.hi = bh.as<float>();
-    a.lo = bl.as<float>();
+    a.mx = bmx.as<float>();
+    a.Rp = Np;
+    a.hi = bh.as<__half>();
+    a.lo = bl.as<__half>();
+    dim3 gmax(ceil_div(g.K, 32), ceil_div(g.N, 32), nzb);
+    rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
+    TN_LAUNCHED();
     dim3 grid(ceil_div(Krp / 2, 32), Nrp / 64, nzb);
     prep_tiled_kernel<1><<<grid, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
   }
-  CUtensorMap mbh = make_map(bh.as<float>(), Krp, Nrp, nzb, TC_BN);
-  CUtensorMap mbl = make_map(bl.as<float>(), Krp, Nrp, nzb, TC_BN);
-  // Split-K when one sample's output has too few tiles to fill the SMs (long-K, small-MN
-  // GEMMs such as the fit derivatives). Chosen from per-sample shapes only (bitwise-identical
-  // results for any batch size); splits are whole promotion chunks.
+  CUtensorMap mbh = make_map(bh.as<__half>(), Krp, Nrp, nzb, TC_BN);
+  CUtensorMap mbl = make_map(bl.as<__half>(), Krp, Nrp, nzb, TC_BN);
+  // ---- split-K when one sample's output has too few tiles to fill the SMs (long-K,
+  // small-MN GEMMs such as the fit derivatives). Chosen from per-sample shapes only
+  // (bitwise-identical results for any batch size); splits are whole promotion chunks.
   const int kblocks = Krp / TC_BK;
   const int mps = g.m_per_sample > 0 ? g.m_per_sample : g.M;
   const int64_t tiles_ps = (int64_t)((mps + TC_BM - 1) / TC_BM) * (Nrp / TC_BN) * g.nb2;
@@ -619,11 +645,12 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     kbps = ((kblocks + ksplit - 1) / ksplit + TC_KC - 1) / TC_KC * TC_KC;
     ksplit = (kblocks + kbps - 1) / kbps;
   }
-  // A planes, chunked over the batch to bound the workspace (<= ~2 GB per plane)
+  // ---- A planes, chunked over the batch to bound the workspace (<= ~1 GB per plane)
   const int64_t per_z = (int64_t)Mp * Krp;
   const int zc = (int)std::max<int64_t>(
       1, std::min<int64_t>({(int64_t)nbz, (int64_t)(65535 / ksplit), (int64_t)(1ll << 29) / std::max<int64_t>(1, per_z)}));
-  DevBuf ah((size_t)zc * per_z * 4, c.stream), al((size_t)zc * per_z * 4, c.stream);
+  DevBuf ah((size_t)zc * per_z * 2, c.stream), al((size_t)zc * per_z * 2, c.stream);
+  DevBuf amx((size_t)zc * Mp * sizeof(float), c.stream);
   DevBuf ws;
   const int64_t ws_split = (int64_t)zc * g.M * g.N;
   if (ksplit > 1) ws.alloc((size_t)ksplit * ws_split * sizeof(float2), c.stream);
@@ -644,14 +671,20 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       a.Rrows = Mp;
       a.Krp = Krp;
       a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
-      a.hi = ah.as<float>();
-      a.lo = al.as<float>();
+      a.mx = amx.as<float>();
+      a.Rp = Mp;
+      a.hi = ah.as<__half>();
+      a.lo = al.as<__half>();
+      TN_CUDA(cudaMemsetAsync(amx.p, 0, (size_t)nz * Mp * sizeof(float), c.stream));
+      dim3 gmax(ceil_div(g.K, 32), ceil_div(g.M, 32), nz);
+      rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
+      TN_LAUNCHED();
       dim3 grid(ceil_div(Krp / 2, 32), Mp / 32, nz);
       prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
       TN_LAUNCHED();
     }
-    CUtensorMap mah = make_map(ah.as<float>(), Krp, Mp, nz, TC_BM);
-    CUtensorMap mal = make_map(al.as<float>(), Krp, Mp, nz, TC_BM);
+    CUtensorMap mah = make_map(ah.as<__half>(), Krp, Mp, nz, TC_BM);
+    CUtensorMap mal = make_map(al.as<__half>(), Krp, Mp, nz, TC_BM);
     TcParams p;
     p.M = g.M;
     p.N = g.N;
@@ -661,6 +694,10 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.ws = ws.as<float2>();
     p.ws_split = ws_split;
     p.b_batched = b_batched ? 1 : 0;
+    p.amax = amx.as<float>();
+    p.bmax = bmx.as<float>() + (b_batched ? (int64_t)z0 * Np : 0);
+    p.Mp = Mp;
+    p.Np = Np;
     p.C = g.C;
     p.cm = g.cm;
     p.nb2 = g.nb2;
@@ -674,9 +711,9 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       ProfScope ps(P_TC_KERNEL, c.stream);
       ++g_tc_launches;
       if (b_batched) {
-        // shift B coordinates by z0: rebuild maps at the chunk's base
-        CUtensorMap mbh2 = make_map(bh.as<float>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
-        CUtensorMap mbl2 = make_map(bl.as<float>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
+        // B planes are indexed by the chunk-relative z: rebuild maps at the chunk's base
+        CUtensorMap mbh2 = make_map(bh.as<__half>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
+        CUtensorMap mbl2 = make_map(bl.as<__half>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
         tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mbh2, mbl2, p);
       } else {
         tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mbh, mbl, p);
