@@ -42,6 +42,7 @@ WORKLOADS = {
     "eagle127_chi16_env64": ("eagle127", 16, 64, 64),
     "square6x6_chi8_env32": ("square6x6", 8, 32, 512),
 }
+PHASES = ["gemm_tc_incl_prep", "gemm_simt", "permute", "orth", "tail", "misc", "tc_kernel"]
 DEFAULT_WORKLOAD = "willow105_chi32_env128"
 STATE_SEED = 2507
 
@@ -290,10 +291,16 @@ def main():
     g = TNState(st)
     t_load = time.time() - t0
     t0 = time.time()
+    pre_prof = np.zeros(7)
+    LIB.tn_debug_set_profile(1)
+    LIB.tn_debug_profile(pre_prof.ctypes.data, None, 7, 1)
     g.prepare(lat.rows, R)
     torch.cuda.synchronize()
     t_pre = time.time() - t0
-    log(f"[rank {rank}] state {t_load:.1f}s, precompute {t_pre:.1f}s")
+    LIB.tn_debug_profile(pre_prof.ctypes.data, None, 7, 1)
+    LIB.tn_debug_set_profile(0)
+    pre_phase = {k: round(float(v), 1) for k, v in zip(PHASES, pre_prof)}
+    log(f"[rank {rank}] state {t_load:.1f}s, precompute {t_pre:.1f}s, phases (ms) {pre_phase}")
 
     N = lat.n
     nsteps = a.warmup + a.steps
@@ -398,8 +405,7 @@ def main():
            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "c64", "data": "synthetic", "config": dict(config, precompute_s=t_pre),
            "roofline": roofline, "e2e": e2e, "gpu_launches": int(cnt[3] - cnt0[3]), "clocks": clk,
-           "phase_ms": {k: float(v) for k, v in zip(["gemm_tc_incl_prep", "gemm_simt", "permute", "orth", "tail",
-                                                      "misc", "tc_kernel"], prof)}}
+           "phase_ms": {k: float(v) for k, v in zip(PHASES, prof)}, "precompute_phase_ms": pre_phase}
     if world == 1 and not a.no_cpu_baseline:
         try:
             out["cpu_baseline"] = oracle_rate(st, lat, R, list(rows), budget_s=a.cpu_budget)
@@ -407,6 +413,8 @@ def main():
             out["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "oracle",
                                    "sample": f"failed: {e}"}
     print(json.dumps(out), flush=True)
+    if os.environ.get("TN_GEMM_LOG"):
+        LIB.tn_debug_gemm_log()
     if dist:
         dist.destroy_process_group()
 

@@ -136,6 +136,19 @@ __device__ __forceinline__ float inv_scale(float mx) {
   return ldexpf(1.f, e);
 }
 
+// Grouped rasterisation: linear tile id -> (m, n), groups of RASTER_GM m-tiles swept with m
+// fastest, so a wave of CTAs shares a few A strips and B strips in L2 instead of streaming
+// one operand strip per CTA from HBM (a full-K strip is 4-8 MB of FP16 planes).
+constexpr int RASTER_GM = 8;
+__device__ __forceinline__ void raster(int lin, int nm, int nn, int& m, int& n) {
+  const int per_group = RASTER_GM * nn;
+  const int g = lin / per_group, r = lin - g * per_group;
+  const int m0 = g * RASTER_GM;
+  const int gm = min(RASTER_GM, nm - m0);
+  m = m0 + r % gm;
+  n = r / gm;
+}
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                    const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo, TcParams p) {
@@ -171,7 +184,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
-  const int nblk = blockIdx.x, mblk = blockIdx.y;
+  const int nblk = blockIdx.x, mblk = blockIdx.y;  // (used for M <= 128 per batch element)
   const int z = blockIdx.z / p.ksplit, split = blockIdx.z - z * p.ksplit;
   const int kb0 = split * p.kb_per_split;
   const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
@@ -294,6 +307,234 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a 256 x 256
+// (real) tile with tcgen05.mma M=256. CTA r loads its own 128 rows of A and rows
+// [128 r, 128 r + 128) of the B^T tile into its shared memory; the leader's single MMA thread
+// reads both CTAs' operands, so each SM streams half of B per MMA -- the shared-memory read
+// traffic per MAC drops by a third against the 1-CTA 128 x 256 tile (the FP16x3 split reads
+// every operand tile twice per k-step, which made the 1-CTA kernel shared-memory bound).
+// Accumulators: each CTA's TMEM holds its 128 rows x 256 columns (two ping-pong buffers).
+constexpr int T2_STAGES = 3;
+constexpr int A2_TILE = 128 * TC_BK * 2;                 // 16 KB per CTA
+constexpr int B2_TILE = 128 * TC_BK * 2;                 // 16 KB per CTA (half of the B tile)
+constexpr int STAGE2_BYTES = 2 * A2_TILE + 2 * B2_TILE;  // 64 KB
+constexpr int SMEM2_BYTES = T2_STAGES * STAGE2_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// TMA load into this CTA's shared memory, completion counted on the leader CTA's mbarrier
+// (bar_cluster = shared::cluster address of that barrier).
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// arrive (once per CTA of the pair) on the barrier at the same offset in both CTAs
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    tc_gemm2_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                    const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo, TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + T2_STAGES * STAGE2_BYTES);
+  uint64_t* empty = full + T2_STAGES;
+  uint64_t* acc_full = empty + T2_STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < T2_STAGES; ++i) {
+      mbar_init(&full[i], 1);   // leader: its producer's arrive.expect_tx (both CTAs' bytes)
+      mbar_init(&empty[i], 1);  // one multicast MMA commit
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 16);  // leader: 8 epilogue warps of each CTA
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAhi)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBhi)));
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  int mpair, nblk;
+  raster(blockIdx.y * (gridDim.x >> 1) + (blockIdx.x >> 1), gridDim.x >> 1, gridDim.y, mpair, nblk);
+  const int mblk = 2 * mpair + (int)rank;
+  const int z = blockIdx.z / p.ksplit, split = blockIdx.z - z * p.ksplit;
+  const int kb0 = split * p.kb_per_split;
+  const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
+  const int nkb = kb1 - kb0;
+  const int bz = p.b_batched ? z : 0;
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs)
+      const uint32_t full0 = map_to_rank(smem_u32(&full[0]), 0);
+      for (int i = 0; i < nkb; ++i) {
+        const int kb = kb0 + i;
+        const int s = i % T2_STAGES;
+        const uint32_t ph = (i / T2_STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * STAGE2_BYTES;
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE2_BYTES);
+        const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
+        tma_load_3d_pair(st, &mAhi, kb * TC_BK, mblk * 128, z, fb);
+        tma_load_3d_pair(st + A2_TILE, &mAlo, kb * TC_BK, mblk * 128, z, fb);
+        tma_load_3d_pair(st + 2 * A2_TILE, &mBhi, kb * TC_BK, nblk * TC_BN + (int)rank * 128, bz, fb);
+        tma_load_3d_pair(st + 2 * A2_TILE + B2_TILE, &mBlo, kb * TC_BK, nblk * TC_BN + (int)rank * 128, bz, fb);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // MMA issuer (leader CTA only)
+      // kind::f16 instruction descriptor: D f32, A/B f16, K-major both, N=256, M=256
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      for (int i = 0; i < nkb; ++i) {
+        const int c = i / TC_KC, buf = c & 1, kin = i - c * TC_KC;
+        if (kin == 0) {
+          mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        const uint32_t dacc = tmem + (uint32_t)(buf * TC_BN);
+        const int s = i % T2_STAGES;
+        const uint32_t ph = (i / T2_STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t base = smem_u32(smem + s * STAGE2_BYTES);
+        const uint64_t ahi = smem_desc(base), alo = smem_desc(base + A2_TILE);
+        const uint64_t bhi = smem_desc(base + 2 * A2_TILE), blo = smem_desc(base + 2 * A2_TILE + B2_TILE);
+#pragma unroll
+        for (int k = 0; k < TC_BK / TC_UK; ++k) {
+          const uint64_t adv = (uint64_t)((k * TC_UK * 2) >> 4);
+          mma_f16_pair(dacc, ahi + adv, bhi + adv, idesc, (kin | k) != 0);
+          mma_f16_pair(dacc, ahi + adv, blo + adv, idesc, 1u);
+          mma_f16_pair(dacc, alo + adv, bhi + adv, idesc, 1u);
+        }
+        mma_commit_pair(&empty[s]);
+        if (kin == TC_KC - 1 || i == nkb - 1) mma_commit_pair(&acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue (both CTAs): warp w drains TMEM lanes 32*(w%4)..+31 (this CTA's rows) and
+    // columns [128*h, 128*h + 128), h = (w-2)/4; chunks are promoted into FP32 registers.
+    const int lg = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int row = mblk * 128 + lg * 32 + lane;
+    const uint32_t acc_empty0 = map_to_rank(smem_u32(&acc_empty[0]), 0);
+    float acc[128];
+#pragma unroll
+    for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+    const int nchunks = (nkb + TC_KC - 1) / TC_KC;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1;
+      mbar_wait(&acc_full[buf], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int cc = 0; cc < 128; cc += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * TC_BN + half * 128 + cc);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[cc + i] += __uint_as_float(v[i]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc_empty0 + (uint32_t)(buf * sizeof(uint64_t)));
+    }
+    if (row < p.M) {
+      const float rs = inv_scale(p.amax[(int64_t)z * p.Mp + row]);
+      const float* bmx = p.bmax + (int64_t)bz * p.Np;
+      const int n0 = (nblk * TC_BN + half * 128) >> 1;
+      if (p.ksplit > 1) {
+        float2* W = p.ws + split * p.ws_split + ((int64_t)z * p.M + row) * p.N;
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          const int n = n0 + q;
+          if (n < p.N) {
+            const float sc = rs * inv_scale(bmx[n]);
+            W[n] = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
+          }
+        }
+      } else {
+        const int b1 = (p.z0 + z) / p.nb2, b2 = (p.z0 + z) - b1 * p.nb2;
+        float2* Crow = p.C + b1 * p.sc1 + b2 * p.sc2 + (int64_t)row * p.cm;
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          const int n = n0 + q;
+          if (n < p.N) {
+            const float sc = rs * inv_scale(bmx[n]);
+            float2 val = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
+            if (p.accumulate) {
+              float2 o = Crow[n];
+              val.x += o.x;
+              val.y += o.y;
+            }
+            Crow[n] = val;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 
@@ -582,10 +823,14 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
   static bool attr = false;
   if (!attr) {
     TN_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    TN_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
     attr = true;
   }
+  // CTA pairs (M = 256 per cluster) whenever one batch element has more than 128 rows
+  static const bool pair_off = getenv("TN_TC2") && std::atoi(getenv("TN_TC2")) == 0;
+  const bool pair = !pair_off && g.M > TC_BM;
   const int Krp = rup(2 * g.K, TC_BK);
-  const int Mp = rup(g.M, TC_BM);
+  const int Mp = rup(g.M, pair ? 2 * TC_BM : TC_BM);
   const int Nrp = rup(2 * g.N, TC_BN);
   const int Np = Nrp / 2;
   const int nbz = g.nb1 * g.nb2;
@@ -629,8 +874,9 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     prep_tiled_kernel<1><<<grid, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
   }
-  CUtensorMap mbh = make_map(bh.as<__half>(), Krp, Nrp, nzb, TC_BN);
-  CUtensorMap mbl = make_map(bl.as<__half>(), Krp, Nrp, nzb, TC_BN);
+  const int bbox = pair ? TC_BN / 2 : TC_BN;
+  CUtensorMap mbh = make_map(bh.as<__half>(), Krp, Nrp, nzb, bbox);
+  CUtensorMap mbl = make_map(bl.as<__half>(), Krp, Nrp, nzb, bbox);
   // ---- split-K when one sample's output has too few tiles to fill the SMs (long-K,
   // small-MN GEMMs such as the fit derivatives). Chosen from per-sample shapes only
   // (bitwise-identical results for any batch size); splits are whole promotion chunks.
@@ -705,18 +951,22 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.sc2 = g.sc2;
     p.z0 = z0;
     p.accumulate = g.accumulate ? 1 : 0;
-    dim3 grid(Nrp / TC_BN, Mp / TC_BM, nz * ksplit);
     if (slog && z0 == 0) cudaEventRecord(srec.b, c.stream);
     {
       ProfScope ps(P_TC_KERNEL, c.stream);
       ++g_tc_launches;
+      CUtensorMap mb_hi = mbh, mb_lo = mbl;
       if (b_batched) {
         // B planes are indexed by the chunk-relative z: rebuild maps at the chunk's base
-        CUtensorMap mbh2 = make_map(bh.as<__half>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
-        CUtensorMap mbl2 = make_map(bl.as<__half>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, TC_BN);
-        tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mbh2, mbl2, p);
+        mb_hi = make_map(bh.as<__half>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, bbox);
+        mb_lo = make_map(bl.as<__half>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, bbox);
+      }
+      if (pair) {
+        dim3 grid(Mp / TC_BM, Nrp / TC_BN, nz * ksplit);  // cluster (2,1,1) pairs M tiles
+        tc_gemm2_kernel<<<grid, TC_THREADS, SMEM2_BYTES, c.stream>>>(mah, mal, mb_hi, mb_lo, p);
       } else {
-        tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mbh, mbl, p);
+        dim3 grid(Nrp / TC_BN, Mp / TC_BM, nz * ksplit);
+        tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mb_hi, mb_lo, p);
       }
       TN_LAUNCHED();
     }
