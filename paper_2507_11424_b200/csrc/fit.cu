@@ -6,6 +6,7 @@
 // re-orthonormalising it (exact D_k columns, R6/R7), the turning site not recomputed,
 // final centre normalised.
 #include <algorithm>
+#include <cstdio>
 
 #include "fit.h"
 #include "kernels.h"
@@ -174,6 +175,23 @@ struct Ops {
   }
 };
 
+}  // namespace
+bool nan_check_on() {
+  static int on = -1;
+  if (on < 0) on = getenv("TN_NAN_CHECK") ? 1 : 0;
+  return on == 1;
+}
+void nan_check(Ctx& c, const char* what, const Tensor& t, int nb) {
+  if (!nan_check_on()) return;
+  int n = t.bstride ? nb : 1;
+  for (int b = 0; b < n; ++b) {
+    int64_t k = count_nonfinite(c, t.p + b * t.bstride, t.size());
+    if (k) fprintf(stderr, "NAN_CHECK %s: sample %d/%d has %lld non-finite of %lld\n", what, b, n, (long long)k,
+                   (long long)t.size());
+  }
+}
+
+namespace {
 // column span of o reshaped (prod(shape[:-1])) x shape[-1]
 Tensor left_orth(Ctx& c, const Tensor& o, int nb) {
   Tensor q = new_tensor_n(c, o.shape, nb);
@@ -182,7 +200,9 @@ Tensor left_orth(Ctx& c, const Tensor& o, int nb) {
   int m = (int)(o.size() / n);
   MatView X{o.p, o.bstride, n, 1, false, m, n};
   MatView Q{q.p, q.bstride, n, 1, false, m, n};
+  nan_check(c, "left_orth in", o, nb);
   orthonormalize(c, X, Q, nullptr, o.bstride ? nb : 1);
+  nan_check(c, "left_orth out", q, nb);
   return q;
 }
 
@@ -200,7 +220,10 @@ Tensor right_orth(Ctx& c, const Tensor& o, int nb, Tensor* Cout) {
     if (!o.bstride) Cout->bstride = 0;
     cp = Cout->p;
   }
+  nan_check(c, "right_orth in", o, nb);
   orthonormalize(c, X, Q, cp, o.bstride ? nb : 1);
+  nan_check(c, "right_orth out", q, nb);
+  if (Cout) nan_check(c, "right_orth C", *Cout, nb);
   return q;
 }
 
@@ -316,6 +339,8 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
           o[k] = view(d, o[k].shape);
           cl = Lk[k];
           cf = Fk[k];
+          nan_check(c, "L env", Lk[k].t, nb);
+          nan_check(c, "F env", Fk[k].t, nb);
         }
         if (k < K - 1) {
           o[k] = left_orth(c, o[k], nb);

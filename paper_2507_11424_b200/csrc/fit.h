@@ -33,6 +33,9 @@ std::vector<int> fit_bonds(const DStrip& s, int R);
 // Fit_R of O3: hash-initialised, gauge-preserving right-orthonormalisation, nh alternating
 // half-sweeps (L->R first), centre site normalised; ln of its norm is written (or added,
 // when accumulate) to logn[b] (device, per sample) if non-null.
+// TN_NAN_CHECK debugging aid (synchronises; no-op unless the variable is set)
+void nan_check(Ctx& c, const char* what, const Tensor& t, int nb);
+
 FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, int nh, double* logn,
               bool accumulate);
 

@@ -128,12 +128,20 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// 1 / s for a row or column maximum mx (s = 2^-e, mx = f 2^e, f in [1/2, 1)).
-__device__ __forceinline__ float inv_scale(float mx) {
-  if (!(mx > 0.f)) return 1.f;
+// Scale exponent of a row or column maximum mx: mx = f 2^e, f in [1/2, 1). Clamped to
+// [-125, 125] so that both s = 2^-e (prep) and 1/s (epilogue) stay finite FP32 numbers: a
+// row of magnitude < 2^-126 (numerical noise, e.g. a null direction of a rank-deficient
+// basis) would otherwise get s = inf and turn the whole output into NaN.
+__device__ __forceinline__ int scale_exp(float mx) {
   int e;
   frexpf(mx, &e);
-  return ldexpf(1.f, e);
+  return max(-125, min(125, e));
+}
+
+// 1 / s for a row or column maximum mx.
+__device__ __forceinline__ float inv_scale(float mx) {
+  if (!(mx > 0.f)) return 1.f;
+  return ldexpf(1.f, scale_exp(mx));
 }
 
 // Grouped rasterisation: linear tile id -> (m, n), groups of RASTER_GM m-tiles swept with m
@@ -645,11 +653,7 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
   if (t < 32) {
     const float m = (r0 + t < a.R) ? a.mx[(int64_t)zz * a.Rp + r0 + t] : 0.f;
     scl[t] = 1.f;
-    if (m > 0.f) {
-      int e;
-      frexpf(m, &e);
-      scl[t] = ldexpf(1.f, -e);
-    }
+    if (m > 0.f) scl[t] = ldexpf(1.f, -scale_exp(m));
   }
   load_tile(a, tile, roff, koff, r0, k0, zz);
   const int64_t plane = (int64_t)a.Rrows * a.Krp;

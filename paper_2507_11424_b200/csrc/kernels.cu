@@ -302,3 +302,24 @@ void scalars_to_host(Ctx& c, const Tensor& t, int nb, std::vector<float2>& out) 
 }
 
 }  // namespace tn
+
+// ---- debugging aid (TN_NAN_CHECK): number of non-finite complex entries of a tensor
+namespace tn {
+namespace {
+__global__ void nonfinite_kernel(const float2* __restrict__ t, int64_t n, unsigned long long* cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float2 v = t[i];
+    if (!isfinite(v.x) || !isfinite(v.y)) atomicAdd(cnt, 1ull);
+  }
+}
+}  // namespace
+int64_t count_nonfinite(Ctx& c, const float2* p, int64_t n) {
+  DevBuf d(sizeof(unsigned long long), c.stream);
+  TN_CUDA(cudaMemsetAsync(d.p, 0, sizeof(unsigned long long), c.stream));
+  if (n > 0) nonfinite_kernel<<<1184, 256, 0, c.stream>>>(p, n, d.as<unsigned long long>());
+  unsigned long long h = 0;
+  TN_CUDA(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+  TN_CUDA(cudaStreamSynchronize(c.stream));
+  return (int64_t)h;
+}
+}  // namespace tn

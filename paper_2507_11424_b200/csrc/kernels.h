@@ -8,6 +8,7 @@ namespace tn {
 void hash_init(Ctx& c, Tensor& o, int nb, uint64_t seed, int tag, int b1, int k);
 
 // Per-sample Frobenius norm: t <- t / ||t||, logn[b] (+)= ln ||t|| when logn != nullptr.
+int64_t count_nonfinite(Ctx& c, const float2* p, int64_t n);  // debugging (synchronises)
 void normalize(Ctx& c, Tensor& t, int nb, double* logn, bool accumulate_log);
 
 // out[b][i] = t[b][0][i] + t[b][1][i]  (sum over a leading axis of size 2)

@@ -1,5 +1,8 @@
 // linalg.cu -- CholeskyQR2 with pivoted rank detection, FP64 arithmetic (see linalg.h).
 #include <algorithm>
+#include <complex>
+#include <cstdio>
+#include <vector>
 
 #include "linalg.h"
 
@@ -331,6 +334,343 @@ __global__ void d2f_kernel(const double2* __restrict__ in, float2* __restrict__ 
     out[e] = make_float2((float)in[e].x, (float)in[e].y);
 }
 
+
+// ======================================================================================
+// Fast path (n <= 128): register-tiled FP64 Gram / apply kernels and a one-CTA-per-matrix
+// Cholesky + triangular inverse entirely in shared memory (lower triangle packed, FP64).
+// The Gram's split count depends only on the matrix shape (results are bitwise independent
+// of the batch size); splits are summed in a fixed order by the Cholesky kernel's load.
+
+constexpr int GT = 64;   // output tile (complex) per CTA, 4 x 4 per thread
+constexpr int GK = 16;   // rows (Gram) / k (apply) per smem chunk
+
+__device__ __forceinline__ float2 mv_ld(const MatView& V, int64_t b, int64_t i, int64_t j) {
+  float2 v = V.p[b * V.bs + i * V.si + j * V.sj];
+  if (V.cj) v.y = -v.y;
+  return v;
+}
+
+// part[b][sp][i][j] = sum over rows r of split sp of conj(Y(r, i)) X(r, j); herm: skip tiles
+// strictly above the diagonal (only the lower triangle i >= j is consumed).
+__global__ void __launch_bounds__(256) gram64_kernel(MatView Y, MatView X, int m, int splits, int herm,
+                                                     const int* __restrict__ rank, int skip_full,
+                                                     double2* __restrict__ part) {
+  const int b = blockIdx.z / splits, sp = blockIdx.z - b * splits;
+  if (rank && skip_full && rank[b] >= X.n) return;
+  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
+  if (herm && i0 + GT <= j0) return;
+  __shared__ double2 sy[GK][GT];
+  __shared__ double2 sx[GK][GT];
+  const int rows_per = (m + splits - 1) / splits;
+  const int r_begin = sp * rows_per, r_end = min(m, r_begin + rows_per);
+  const int t = threadIdx.x, ty = t >> 4, tx = t & 15;
+  const bool yrow = (Y.si == 1 && Y.sj != 1), xrow = (X.si == 1 && X.sj != 1);
+  double2 acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = make_double2(0, 0);
+  for (int r0 = r_begin; r0 < r_end; r0 += GK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = t + 256 * q;
+      int rr = yrow ? (e & 15) : (e >> 6), cc = yrow ? (e >> 4) : (e & 63);
+      int r = r0 + rr;
+      float2 v = make_float2(0.f, 0.f);
+      if (r < r_end && i0 + cc < Y.n) v = mv_ld(Y, b, r, i0 + cc);
+      sy[rr][cc] = make_double2((double)v.x, (double)v.y);
+      rr = xrow ? (e & 15) : (e >> 6);
+      cc = xrow ? (e >> 4) : (e & 63);
+      r = r0 + rr;
+      v = make_float2(0.f, 0.f);
+      if (r < r_end && j0 + cc < X.n) v = mv_ld(X, b, r, j0 + cc);
+      sx[rr][cc] = make_double2((double)v.x, (double)v.y);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < GK; ++rr) {
+      double2 yv[4], xv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) yv[a] = sy[rr][ty * 4 + a];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) xv[c] = sx[rr][tx + 16 * c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          // conj(y) * x
+          acc[a][c].x = fma(yv[a].x, xv[c].x, fma(yv[a].y, xv[c].y, acc[a][c].x));
+          acc[a][c].y = fma(yv[a].x, xv[c].y, fma(-yv[a].y, xv[c].x, acc[a][c].y));
+        }
+    }
+    __syncthreads();
+  }
+  const int nI = Y.n, nJ = X.n;
+  double2* out = part + ((int64_t)b * splits + sp) * nI * nJ;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + ty * 4 + a, j = j0 + tx + 16 * c;
+      if (i < nI && j < nJ) out[(int64_t)i * nJ + j] = acc[a][c];
+    }
+}
+
+// O(i, j) = sum_k X(i, k) W[b][k][j]  (X FP32 view, W FP64 [n][n], O FP32 view)
+__global__ void __launch_bounds__(256) apply64v_kernel(MatView X, const double2* __restrict__ Wall, MatView O,
+                                                       const int* __restrict__ rank, int skip_full) {
+  const int b = blockIdx.z;
+  const int m = X.m, n = X.n;
+  if (rank && skip_full && rank[b] >= n) return;
+  __shared__ double2 sa[GT][GK + 1];
+  __shared__ double2 sw[GK][GT];
+  const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
+  const double2* W = Wall + (int64_t)b * n * n;
+  const int t = threadIdx.x, ty = t >> 4, tx = t & 15;
+  const bool xrow = (X.si == 1 && X.sj != 1);
+  double2 acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = make_double2(0, 0);
+  for (int k0 = 0; k0 < n; k0 += GK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = t + 256 * q;
+      const int ii = xrow ? (e & 63) : (e >> 4), kk = xrow ? (e >> 6) : (e & 15);
+      const int i = i0 + ii, k = k0 + kk;
+      float2 v = make_float2(0.f, 0.f);
+      if (i < m && k < n) v = mv_ld(X, b, i, k);
+      sa[ii][kk] = make_double2((double)v.x, (double)v.y);
+      const int kk2 = e >> 6, jj = e & 63;
+      sw[kk2][jj] = (k0 + kk2 < n && j0 + jj < n) ? W[(int64_t)(k0 + kk2) * n + j0 + jj] : make_double2(0, 0);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < GK; ++kk) {
+      double2 av[4], wv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = sa[ty * 4 + a][kk];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) wv[c] = sw[kk][tx + 16 * c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[a][c].x = fma(av[a].x, wv[c].x, fma(-av[a].y, wv[c].y, acc[a][c].x));
+          acc[a][c].y = fma(av[a].x, wv[c].y, fma(av[a].y, wv[c].x, acc[a][c].y));
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + ty * 4 + a, j = j0 + tx + 16 * c;
+      if (i < m && j < n) {
+        float2 v = make_float2((float)acc[a][c].x, (float)(O.cj ? -acc[a][c].y : acc[a][c].y));
+        O.p[b * O.bs + (int64_t)i * O.si + (int64_t)j * O.sj] = v;
+      }
+    }
+}
+
+constexpr int CH_MAXN = 128;
+constexpr int CH_THREADS = 1024;
+constexpr size_t CH_SMEM = (size_t)CH_MAXN * (CH_MAXN + 1) / 2 * sizeof(double2)  // packed lower G / L
+                           + (size_t)(CH_THREADS / 32) * CH_MAXN * sizeof(double2)   // per-warp y columns
+                           + (size_t)CH_MAXN * sizeof(double2)                       // l vector
+                           + (size_t)CH_MAXN * (sizeof(double) + 2 * sizeof(int)) + 64;
+
+__device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // i >= j
+
+// Cholesky G = L L^H of each Hermitian n x n matrix (G summed from `splits` Gram partials),
+// then W = P L^{-H} so that Q = X W. PIVOT: symmetric pivoting on the largest remaining
+// diagonal with rank detection (diag <= tol * max initial diag stops; rank < n matrices get
+// no W -- the completion path handles them). Without PIVOT, tiny pivots are clamped and
+// flagged in *bad. Everything lives in shared memory (packed lower triangle in FP64).
+template <bool PIVOT>
+__global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __restrict__ part, int splits, int n,
+                                                               double tol, double2* __restrict__ Wall,
+                                                               int* __restrict__ perm_all, int* __restrict__ rank_all,
+                                                               double* __restrict__ dmax_all, int* __restrict__ bad,
+                                                               const int* __restrict__ rank_in, int skip_full) {
+  extern __shared__ double2 chs[];
+  const int b = blockIdx.x;
+  if (rank_in && skip_full && rank_in[b] >= n) return;
+  double2* S = chs;                                       // packed lower, original indices
+  double2* Y = S + CH_MAXN * (CH_MAXN + 1) / 2;           // [32 warps][CH_MAXN]
+  double2* lv = Y + (CH_THREADS / 32) * CH_MAXN;          // [CH_MAXN]
+  double* dg = reinterpret_cast<double*>(lv + CH_MAXN);   // [CH_MAXN] diagonal
+  int* alive = reinterpret_cast<int*>(dg + CH_MAXN);      // [CH_MAXN]
+  int* perm = alive + CH_MAXN;                            // [CH_MAXN]
+  __shared__ int s_piv, s_rank;
+  __shared__ double s_dp, s_d0;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int64_t nn = (int64_t)n * n;
+  const double2* P0 = part + (int64_t)b * splits * nn;
+  // load the lower triangle (sum of the split partials, fixed order)
+  for (int i = warp; i < n; i += CH_THREADS / 32)
+    for (int j = lane; j <= i; j += 32) {
+      double2 s = P0[(int64_t)i * n + j];
+      for (int k = 1; k < splits; ++k) {
+        double2 v = P0[k * nn + (int64_t)i * n + j];
+        s.x += v.x;
+        s.y += v.y;
+      }
+      S[pk(i, j)] = s;
+      if (i == j) dg[i] = s.x;
+    }
+  for (int i = t; i < n; i += CH_THREADS) {
+    alive[i] = 1;
+    perm[i] = i;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double mx = 0;
+    for (int i = lane; i < n; i += 32) mx = fmax(mx, dg[i]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+      s_d0 = mx;
+      s_rank = n;
+    }
+  }
+  __syncthreads();
+  const double d0 = s_d0;
+  const double floor_d = 1e-300 + 1e-30 * d0;
+  for (int k = 0; k < n; ++k) {
+    if (warp == 0) {
+      int p = k;
+      double dp;
+      if (PIVOT) {
+        double bv = -1;
+        int bi = n;
+        for (int i = lane; i < n; i += 32)
+          if (alive[i] && dg[i] > bv) {
+            bv = dg[i];
+            bi = i;
+          }
+        for (int o = 16; o > 0; o >>= 1) {
+          double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        p = bi;
+        dp = bv;
+      } else {
+        dp = dg[k];
+      }
+      if (lane == 0) {
+        s_piv = p;
+        s_dp = dp;
+      }
+    }
+    __syncthreads();
+    const int p = s_piv;
+    double dp = s_dp;
+    if (PIVOT) {
+      if (!(dp > tol * d0) || d0 <= 0) {
+        if (t == 0) s_rank = k;
+        break;
+      }
+    } else if (!(dp > floor_d)) {
+      if (t == 0) atomicOr(bad, 1);
+      dp = floor_d;
+    }
+    const double lkk = sqrt(dp);
+    const double inv = 1.0 / lkk;
+    // column of L for the remaining indices: l_i = G(i, p) / lkk (stored back in place)
+    for (int i = t; i < n; i += CH_THREADS) {
+      if (i == p) {
+        S[pk(p, p)] = make_double2(lkk, 0);
+        lv[i] = make_double2(0, 0);
+      } else if (alive[i]) {
+        double2 g = i > p ? S[pk(i, p)] : S[pk(p, i)];
+        if (i < p) g.y = -g.y;  // G(i, p) = conj(G(p, i))
+        double2 l = make_double2(g.x * inv, g.y * inv);
+        lv[i] = l;
+        if (i > p) S[pk(i, p)] = l;
+        else S[pk(p, i)] = make_double2(l.x, -l.y);
+      } else {
+        lv[i] = make_double2(0, 0);
+      }
+    }
+    __syncthreads();
+    if (t == 0) {
+      alive[p] = 0;
+      perm[k] = p;
+    }
+    // Schur complement on the remaining indices (lower triangle): G(i,j) -= l_i conj(l_j)
+    for (int i = warp; i < n; i += CH_THREADS / 32) {
+      if (i == p || !alive[i]) continue;
+      const double2 li = lv[i];
+      for (int j = lane; j <= i; j += 32) {
+        if (j == p || !alive[j]) continue;
+        const double2 lj = lv[j];
+        double2 g = S[pk(i, j)];
+        g.x -= li.x * lj.x + li.y * lj.y;
+        g.y -= li.y * lj.x - li.x * lj.y;
+        S[pk(i, j)] = g;
+        if (i == j) dg[i] = g.x;
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  const int rank = s_rank;
+  if (PIVOT && t == 0) {
+    rank_all[b] = rank;
+    dmax_all[b] = d0;
+  }
+  if (PIVOT) {
+    for (int i = t; i < n; i += CH_THREADS) perm_all[(int64_t)b * n + i] = perm[i];
+    if (rank < n) return;  // completion path
+  }
+  // L(i, k) in pivot order = G(perm[i], perm[k]) (i > k); L(k, k) = G(perm[k], perm[k]).
+  // Linv column j by forward substitution (one warp per column), W[perm[k]][j] = conj(Linv[j][k]).
+  double2* W = Wall + (int64_t)b * nn;
+  double2* y = Y + warp * CH_MAXN;
+  for (int jj = warp; jj < n; jj += CH_THREADS / 32) {
+    // balance: warp w takes columns w, 2*32-1-w, ... (long and short columns)
+    const int blk = jj / (CH_THREADS / 32), w = jj % (CH_THREADS / 32);
+    const int sz = min(CH_THREADS / 32, n - blk * (CH_THREADS / 32));
+    const int j = (blk & 1) ? blk * (CH_THREADS / 32) + (sz - 1 - w) : jj;
+    const int pj = perm[j];
+    if (lane == 0) y[j] = make_double2(1.0 / S[pk(pj, pj)].x, 0);
+    __syncwarp();
+    for (int i = j + 1; i < n; ++i) {
+      const int pi = perm[i];
+      double sx = 0, sy = 0;
+      for (int k = j + lane; k < i; k += 32) {
+        const int pkk = perm[k];
+        double2 l = pi > pkk ? S[pk(pi, pkk)] : S[pk(pkk, pi)];
+        if (pi < pkk) l.y = -l.y;
+        const double2 yk = y[k];
+        sx += l.x * yk.x - l.y * yk.y;
+        sy += l.x * yk.y + l.y * yk.x;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      }
+      if (lane == 0) {
+        const double lii = S[pk(pi, pi)].x;
+        y[i] = make_double2(-sx / lii, -sy / lii);
+      }
+      __syncwarp();
+    }
+    // y = Linv(:, j); W = P L^-H: W[perm[j]][k] = conj(Linv(k, j))
+    for (int k = lane; k < n; k += 32) {
+      double2 v = k >= j ? make_double2(y[k].x, -y[k].y) : make_double2(0, 0);
+      W[(int64_t)pj * n + k] = v;
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 // out[b] = Y^H X  (n_Y x n_X), fp64
@@ -350,11 +690,157 @@ static void cross64(Ctx& c, const MatView& Y, const MatView& X, int m, int nb, d
   TN_LAUNCHED();
 }
 
+
+static bool getenv_flag(const char* k) {
+  const char* v = getenv(k);
+  return v && *v && *v != '0';
+}
+
+// shape-only split count (determinism across batch sizes)
+static int gram_splits(int m, int nI, int nJ) {
+  int tiles = (int)(ceil_div(nI, GT) * ceil_div(nJ, GT));
+  int want = (2 * 148 + tiles - 1) / tiles;
+  return std::max(1, std::min({want, std::max(1, m / 128), 64}));
+}
+
+static void gram(Ctx& c, const MatView& Y, const MatView& X, int m, int nb, bool herm, const int* rank,
+                 int skip_full, DevBuf& part, int& splits) {
+  splits = gram_splits(m, Y.n, X.n);
+  size_t need = (size_t)nb * splits * Y.n * X.n * sizeof(double2);
+  if (part.bytes < need) part.alloc(need, c.stream);
+  dim3 grid(ceil_div(X.n, GT), ceil_div(Y.n, GT), (unsigned)(nb * splits));
+  gram64_kernel<<<grid, 256, 0, c.stream>>>(Y, X, m, splits, herm ? 1 : 0, rank, skip_full, part.as<double2>());
+  TN_LAUNCHED();
+}
+
+static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, int nb) {
+  const int m = X.m, n = X.n;
+  static bool attr = false;
+  if (!attr) {
+    TN_CUDA(cudaFuncSetAttribute(chol_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CH_SMEM));
+    TN_CUDA(cudaFuncSetAttribute(chol_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CH_SMEM));
+    attr = true;
+  }
+  const size_t nn = (size_t)n * n * nb;
+  DevBuf part, W(nn * sizeof(double2), c.stream);
+  DevBuf perm((size_t)n * nb * sizeof(int), c.stream), rank((size_t)nb * sizeof(int), c.stream);
+  DevBuf dmax((size_t)nb * sizeof(double), c.stream), bad(sizeof(int), c.stream);
+  DevBuf Q1((size_t)m * n * nb * sizeof(float2), c.stream);
+  TN_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
+  MatView Q1v{Q1.as<float2>(), (int64_t)m * n, n, 1, false, m, n};
+  const dim3 agrid(ceil_div(n, GT), ceil_div(m, GT), nb);
+  int splits = 1;
+  // pass 1: G = X^H X, pivoted Cholesky (rank detection); full rank: Q1 = X P L^-H
+  gram(c, X, X, m, nb, true, nullptr, 0, part, splits);
+  static const double tol = getenv("TN_ORTH_TOL") ? atof(getenv("TN_ORTH_TOL")) : 1e-13;
+  chol_smem_kernel<true><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, tol,
+                                                                W.as<double2>(), perm.as<int>(), rank.as<int>(),
+                                                                dmax.as<double>(), bad.as<int>(), nullptr, 0);
+  TN_LAUNCHED();
+  apply64v_kernel<<<agrid, 256, 0, c.stream>>>(X, W.as<double2>(), Q1v, nullptr, 0);
+  TN_LAUNCHED();
+  // rank-deficient matrices only (every kernel returns at once for full-rank ones):
+  // X' = [X P(:, :r), Y] -> Cholesky -> Q1 = X' R'^-1
+  {
+    DevBuf Ap((size_t)m * n * nb * sizeof(float2), c.stream);
+    int64_t tot = (int64_t)m * n * nb;
+    unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16);
+    build_aprime<<<blocks, 256, 0, c.stream>>>(X, Ap.as<float2>(), perm.as<int>(), rank.as<int>(),
+                                               dmax.as<double>(), nb);
+    TN_LAUNCHED();
+    MatView Av{Ap.as<float2>(), (int64_t)m * n, n, 1, false, m, n};
+    gram(c, Av, Av, m, nb, true, rank.as<int>(), 1, part, splits);
+    chol_smem_kernel<false><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, 0.0,
+                                                                   W.as<double2>(), perm.as<int>(), rank.as<int>(),
+                                                                   dmax.as<double>(), bad.as<int>(), rank.as<int>(), 1);
+    TN_LAUNCHED();
+    apply64v_kernel<<<agrid, 256, 0, c.stream>>>(Av, W.as<double2>(), Q1v, rank.as<int>(), 1);
+    TN_LAUNCHED();
+  }
+  // pass 2 (re-orthogonalisation): G2 = Q1^H Q1 -> Q = Q1 R2^-1
+  gram(c, Q1v, Q1v, m, nb, true, nullptr, 0, part, splits);
+  chol_smem_kernel<false><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, 0.0,
+                                                                 W.as<double2>(), perm.as<int>(), nullptr,
+                                                                 nullptr, bad.as<int>(), nullptr, 0);
+  TN_LAUNCHED();
+  apply64v_kernel<<<agrid, 256, 0, c.stream>>>(Q1v, W.as<double2>(), Q, nullptr, 0);
+  TN_LAUNCHED();
+  if (Cout) {
+    gram(c, Q, X, m, nb, false, nullptr, 0, part, splits);
+    int64_t per = (int64_t)n * n;
+    unsigned blocks = (unsigned)std::min<int64_t>((per * nb + 255) / 256, 4096);
+    reduce_splits<<<blocks, 256, 0, c.stream>>>(part.as<double2>(), W.as<double2>(), splits, per, nb);
+    TN_LAUNCHED();
+    unsigned b2 = (unsigned)std::min<int64_t>(((int64_t)nn + 255) / 256, 4096);
+    d2f_kernel<<<b2, 256, 0, c.stream>>>(W.as<double2>(), Cout, (int64_t)nn);
+    TN_LAUNCHED();
+  }
+}
+
+
+// TN_ORTH_CHECK=1 (debugging only): host-side check of Q^H Q = I and X = Q Q^H X.
+static void orth_check(Ctx& c, const MatView& X, const MatView& Q, int nb) {
+  TN_CUDA(cudaStreamSynchronize(c.stream));
+  const int m = X.m, n = X.n;
+  auto fetch = [&](const MatView& V, int b, std::vector<std::complex<double>>& out) {
+    int64_t lo = INT64_MAX, hi = 0;
+    for (int64_t i : {(int64_t)0, (int64_t)m - 1})
+      for (int64_t j : {(int64_t)0, (int64_t)n - 1}) {
+        int64_t o = b * V.bs + i * V.si + j * V.sj;
+        lo = std::min(lo, o);
+        hi = std::max(hi, o);
+      }
+    std::vector<float2> h(hi - lo + 1);
+    TN_CUDA(cudaMemcpy(h.data(), V.p + lo, h.size() * sizeof(float2), cudaMemcpyDeviceToHost));
+    out.assign((size_t)m * n, 0);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < n; ++j) {
+        float2 v = h[b * V.bs + (int64_t)i * V.si + (int64_t)j * V.sj - lo];
+        out[(size_t)i * n + j] = std::complex<double>(v.x, V.cj ? -v.y : v.y);
+      }
+  };
+  for (int b = 0; b < nb; ++b) {
+    std::vector<std::complex<double>> x, q;
+    fetch(X, b, x);
+    fetch(Q, b, q);
+    double orth = 0, xn = 0, res = 0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        std::complex<double> s = 0;
+        for (int r = 0; r < m; ++r) s += std::conj(q[(size_t)r * n + i]) * q[(size_t)r * n + j];
+        orth = std::max(orth, std::abs(s - (i == j ? 1.0 : 0.0)));
+      }
+    std::vector<std::complex<double>> c2((size_t)n * n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        std::complex<double> s = 0;
+        for (int r = 0; r < m; ++r) s += std::conj(q[(size_t)r * n + i]) * x[(size_t)r * n + j];
+        c2[(size_t)i * n + j] = s;
+      }
+    for (int r = 0; r < m; ++r)
+      for (int j = 0; j < n; ++j) {
+        std::complex<double> s = 0;
+        for (int i = 0; i < n; ++i) s += q[(size_t)r * n + i] * c2[(size_t)i * n + j];
+        res += std::norm(x[(size_t)r * n + j] - s);
+        xn += std::norm(x[(size_t)r * n + j]);
+      }
+    double rel = std::sqrt(res / std::max(xn, 1e-300));
+    if (orth > 1e-4 || rel > 1e-4 || !std::isfinite(orth) || !std::isfinite(rel))
+      fprintf(stderr, "ORTH_CHECK m=%d n=%d b=%d/%d: |QhQ-I|=%.3e |X-QQhX|/|X|=%.3e |X|=%.3e\n", m, n, b, nb, orth, rel,
+              std::sqrt(xn));
+  }
+}
+
 void orthonormalize(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, int nb) {
   int m = X.m, n = X.n;
   if (n == 0 || nb == 0) return;
   if (m < n) throw Error(-1, "orthonormalize: more columns than rows");
   ProfScope ps(P_ORTH, c.stream);
+  if (n <= CH_MAXN && !getenv_flag("TN_ORTH_OLD")) {
+    orth_fast(c, X, Q, Cout, nb);
+    if (getenv_flag("TN_ORTH_CHECK")) orth_check(c, X, Q, nb);
+    return;
+  }
   size_t nn = (size_t)n * n * nb;
   DevBuf G(nn * sizeof(double2), c.stream), W(nn * sizeof(double2), c.stream);
   DevBuf perm((size_t)n * nb * sizeof(int), c.stream), rank((size_t)nb * sizeof(int), c.stream);

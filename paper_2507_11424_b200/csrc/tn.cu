@@ -232,7 +232,16 @@ Envs& norm_envs(tn_state* st, Layout& L, int R) {
   E.logs.assign(nbr, 0.0);
   DevBuf logd(sizeof(double) * nbr, c.stream);
   TN_CUDA(cudaMemsetAsync(logd.p, 0, sizeof(double) * nbr, c.stream));
+  // TN_PRE_ROWS=k (profiling only): stop after the k bottom-most fits; the environments are
+  // then incomplete and not marked ready.
+  const char* lim_s = getenv("TN_PRE_ROWS");
+  const int lim = lim_s ? std::atoi(lim_s) : -1;
   for (int b = nbr - 1; b >= 1; --b) {
+    if (lim >= 0 && nbr - 1 - b >= lim) {
+      TN_CUDA(cudaStreamSynchronize(c.stream));
+      st->last_precompute_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return E;
+    }
     DStrip s;
     s.dbl = true;
     s.per_sample = false;
@@ -312,6 +321,7 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
       s.out.push_back(true);
     }
     FitResult fr = fit(c, s, R, 1, b + 1, st->seed, st->nh, nullptr, false);
+    for (int j = 0; j < W; ++j) nan_check(c, ("n site row " + std::to_string(b) + " j " + std::to_string(j)).c_str(), fr.sites[j], nb);
     std::vector<Tensor> n(W);
     for (int j = 0; j < W; ++j) {
       const Tensor& o = fr.sites[j];
@@ -330,6 +340,7 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
       if (ms.tops[j].p) Y2 = contract(c, Y1, "asdfZ", false, ms.tops[j], "edDf", false, "asZeD");
       else Y2 = permute(c, Y1, "asdfZ", "asZfd");  // identity: e = f, d = D = 1
       Rs[j] = contract(c, Y2, "asZeD", false, n[j], "AsDZ", true, "saeA");
+      nan_check(c, ("Rs row " + std::to_string(b) + " j " + std::to_string(j)).c_str(), Rs[j], nb);
       if (j > 0) {
         Rr = sum2(c, Rs[j]);
         normalize(c, Rr, nb, nullptr, false);  // any positive rescale (R13)
@@ -351,7 +362,9 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
         if (ms.tops[j].p) G2 = contract(c, G1, "eAdz", false, ms.tops[j], "edDf", false, "AzDf");
         else G2 = permute(c, G1, "eAdz", "Azde");  // identity: f = e, d = D = 1
         Lx = contract(c, G2, "AzDf", false, nx, "ADZ", true, "zfZ");
+        nan_check(c, ("Lx pre-norm row " + std::to_string(b) + " j " + std::to_string(j)).c_str(), Lx, nb);
         normalize(c, Lx, nb, nullptr, false);
+        nan_check(c, ("Lx row " + std::to_string(b) + " j " + std::to_string(j)).c_str(), Lx, nb);
       }
     }
     // a5: m_b = merge(n_b[x_b]) -- vertices without a down edge are multiplied into the

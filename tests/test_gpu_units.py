@@ -107,6 +107,20 @@ def test_contract_gather_views(gemm):
     assert close(out, ref)
 
 
+def test_contract_tiny_rows_tensor_core():
+    """Rows/columns of magnitude ~1e-40 (FP32 subnormal) next to O(1) ones: the FP16x3 path's
+    power-of-two scaling must stay finite (a scale of 2^139 once overflowed to inf -> NaN)."""
+    rng = np.random.default_rng(9)
+    A = rand(rng, (256, 512))
+    B = rand(rng, (512, 256))
+    A[3] *= 1e-40
+    A[7] = 0
+    B[:, 5] *= 1e-40
+    out, ref = dcontract(A, "mk", B, "kn", "mn", gemm=2)
+    assert np.isfinite(out).all()
+    assert np.abs(out - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
 def test_contract_large_k():
     rng = np.random.default_rng(2)
     out, ref = dcontract(rand(rng, (130, 1000)), "ak", rand(rng, (1000, 70)), "kb", "ab")
@@ -153,6 +167,36 @@ def test_orth_rank_deficient():
         assert np.abs(q.conj().T @ q - np.eye(n)).max() < 1e-5
         x = X[b].astype(np.complex128)
         assert np.linalg.norm(x - q @ (q.conj().T @ x)) <= 1e-5 * max(1e-30, np.linalg.norm(x))
+
+
+@pytest.mark.parametrize("transpose", [False, True])
+def test_orth_mixed_batch(transpose):
+    """One launch over a batch mixing full-rank, exactly rank-deficient, numerically
+    rank-deficient (FP32-level noise on a rank-3 matrix) and zero matrices: every basis is
+    orthonormal, contains span(X), and C reproduces X."""
+    rng = np.random.default_rng(6)
+    m, n = 1024, 16
+    X = rand(rng, (5, m, n)).astype(np.complex128)
+    X[1] = rand(rng, (m, 3)) @ rand(rng, (3, n))
+    X[2] = rand(rng, (m, 3)) @ rand(rng, (3, n))
+    X[2] += 3e-6 * np.abs(X[2]).max() * rand(rng, (m, n))
+    X[3] = 0
+    X[4] *= 1e12
+    if transpose:
+        X = np.ascontiguousarray(np.swapaxes(X, 1, 2))
+    Q, Cm = _orth(X.astype(np.complex64), transpose=transpose)
+    for b in range(5):
+        q = Q[b].astype(np.complex128)
+        x = X[b].astype(np.complex64).astype(np.complex128)
+        assert np.isfinite(q).all() and np.isfinite(Cm[b]).all(), b
+        if transpose:
+            q, x, c = q.T, x.T, Cm[b].conj()
+        else:
+            c = Cm[b]
+        assert np.abs(q.conj().T @ q - np.eye(n)).max() < 1e-5, b
+        nx = max(1e-30, np.linalg.norm(x))
+        assert np.linalg.norm(x - q @ (q.conj().T @ x)) <= 1e-5 * nx, b
+        assert np.linalg.norm(x - q @ c.astype(np.complex128)) <= 1e-5 * nx, b
 
 
 def test_orth_rows():
