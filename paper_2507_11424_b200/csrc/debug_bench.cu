@@ -24,6 +24,16 @@ extern "C" int tn_debug_gemm_bench(int M, int N, int K, int nb, int mode, int re
     TN_CUDA(cudaStreamCreate(&c.stream));
     c.nb = nb;
     c.gemm_mode = mode;
+    {
+      // as tn_load_state: keep freed blocks in the pool (otherwise every synchronisation
+      // returns GBs to the OS and the next call re-maps them inside the timed region)
+      int dev = 0;
+      cudaMemPool_t pool;
+      TN_CUDA(cudaGetDevice(&dev));
+      TN_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t thr = UINT64_MAX;
+      TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     double ms = 0, err = 0;
     {
       Tensor A = new_tensor(c, {M, K}, true), B = new_tensor(c, {K, N}, false);

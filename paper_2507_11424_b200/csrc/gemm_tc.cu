@@ -381,9 +381,32 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
+// Persistent: a grid of at most 74 CTA pairs walks the tile space (batch element, K split,
+// M pair-tile, N tile) with a static stride; the TMA ring, the MMA's TMEM ping-pong and the
+// epilogue run continuously across tiles, so one tile's epilogue overlaps the next tile's
+// main loop and the prologue (barrier init, TMEM allocation) is paid once per CTA.
+struct PairTile {
+  int z, split, mblk0, nblk, kb0, nkb;
+};
+
+__device__ __forceinline__ PairTile pair_tile(const TcParams& p, int t, int npm, int nn) {
+  PairTile r;
+  const int per_z = npm * nn;
+  const int zs = t / per_z, rem = t - zs * per_z;
+  r.z = zs / p.ksplit;
+  r.split = zs - r.z * p.ksplit;
+  int mpair;
+  raster(rem, npm, nn, mpair, r.nblk);
+  r.mblk0 = 2 * mpair;
+  r.kb0 = r.split * p.kb_per_split;
+  r.nkb = min(p.kblocks, r.kb0 + p.kb_per_split) - r.kb0;
+  return r;
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
-                    const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo, TcParams p) {
+                    const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo, TcParams p,
+                    int npm, int nn, int ntiles) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + T2_STAGES * STAGE2_BYTES);
@@ -394,6 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < T2_STAGES; ++i) {
       mbar_init(&full[i], 1);   // leader: its producer's arrive.expect_tx (both CTAs' bytes)
@@ -417,29 +441,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
-  int mpair, nblk;
-  raster(blockIdx.y * (gridDim.x >> 1) + (blockIdx.x >> 1), gridDim.x >> 1, gridDim.y, mpair, nblk);
-  const int mblk = 2 * mpair + (int)rank;
-  const int z = blockIdx.z / p.ksplit, split = blockIdx.z - z * p.ksplit;
-  const int kb0 = split * p.kb_per_split;
-  const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
-  const int nkb = kb1 - kb0;
-  const int bz = p.b_batched ? z : 0;
   if (warp == 0) {
     if (lane == 0) {  // TMA producer (both CTAs)
       const uint32_t full0 = map_to_rank(smem_u32(&full[0]), 0);
-      for (int i = 0; i < nkb; ++i) {
-        const int kb = kb0 + i;
-        const int s = i % T2_STAGES;
-        const uint32_t ph = (i / T2_STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* st = smem + s * STAGE2_BYTES;
-        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE2_BYTES);
-        const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
-        tma_load_3d_pair(st, &mAhi, kb * TC_BK, mblk * 128, z, fb);
-        tma_load_3d_pair(st + A2_TILE, &mAlo, kb * TC_BK, mblk * 128, z, fb);
-        tma_load_3d_pair(st + 2 * A2_TILE, &mBhi, kb * TC_BK, nblk * TC_BN + (int)rank * 128, bz, fb);
-        tma_load_3d_pair(st + 2 * A2_TILE + B2_TILE, &mBlo, kb * TC_BK, nblk * TC_BN + (int)rank * 128, bz, fb);
+      int i = 0;  // running stage counter
+      for (int t = cluster; t < ntiles; t += nclusters) {
+        const PairTile tl = pair_tile(p, t, npm, nn);
+        const int mrow = (tl.mblk0 + (int)rank) * 128;
+        const int brow = tl.nblk * TC_BN + (int)rank * 128;
+        const int bz = p.b_batched ? tl.z : 0;
+        for (int q = 0; q < tl.nkb; ++q, ++i) {
+          const int kb = tl.kb0 + q;
+          const int s = i % T2_STAGES;
+          const uint32_t ph = (i / T2_STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * STAGE2_BYTES;
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE2_BYTES);
+          const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
+          tma_load_3d_pair(st, &mAhi, kb * TC_BK, mrow, tl.z, fb);
+          tma_load_3d_pair(st + A2_TILE, &mAlo, kb * TC_BK, mrow, tl.z, fb);
+          tma_load_3d_pair(st + 2 * A2_TILE, &mBhi, kb * TC_BK, brow, bz, fb);
+          tma_load_3d_pair(st + 2 * A2_TILE + B2_TILE, &mBlo, kb * TC_BK, brow, bz, fb);
+        }
       }
     }
     __syncwarp();
@@ -447,29 +470,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     if (lane == 0 && rank == 0) {  // MMA issuer (leader CTA only)
       // kind::f16 instruction descriptor: D f32, A/B f16, K-major both, N=256, M=256
       const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-      for (int i = 0; i < nkb; ++i) {
-        const int c = i / TC_KC, buf = c & 1, kin = i - c * TC_KC;
-        if (kin == 0) {
-          mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
+      int i = 0, c = 0;  // running stage and chunk counters
+      for (int t = cluster; t < ntiles; t += nclusters) {
+        const PairTile tl = pair_tile(p, t, npm, nn);
+        for (int q = 0; q < tl.nkb; ++q, ++i) {
+          const int kin = q % TC_KC, buf = c & 1;
+          if (kin == 0) {
+            mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+          }
+          const uint32_t dacc = tmem + (uint32_t)(buf * TC_BN);
+          const int s = i % T2_STAGES;
+          const uint32_t ph = (i / T2_STAGES) & 1;
+          mbar_wait(&full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
-        }
-        const uint32_t dacc = tmem + (uint32_t)(buf * TC_BN);
-        const int s = i % T2_STAGES;
-        const uint32_t ph = (i / T2_STAGES) & 1;
-        mbar_wait(&full[s], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t base = smem_u32(smem + s * STAGE2_BYTES);
-        const uint64_t ahi = smem_desc(base), alo = smem_desc(base + A2_TILE);
-        const uint64_t bhi = smem_desc(base + 2 * A2_TILE), blo = smem_desc(base + 2 * A2_TILE + B2_TILE);
+          const uint32_t base = smem_u32(smem + s * STAGE2_BYTES);
+          const uint64_t ahi = smem_desc(base), alo = smem_desc(base + A2_TILE);
+          const uint64_t bhi = smem_desc(base + 2 * A2_TILE), blo = smem_desc(base + 2 * A2_TILE + B2_TILE);
 #pragma unroll
-        for (int k = 0; k < TC_BK / TC_UK; ++k) {
-          const uint64_t adv = (uint64_t)((k * TC_UK * 2) >> 4);
-          mma_f16_pair(dacc, ahi + adv, bhi + adv, idesc, (kin | k) != 0);
-          mma_f16_pair(dacc, ahi + adv, blo + adv, idesc, 1u);
-          mma_f16_pair(dacc, alo + adv, bhi + adv, idesc, 1u);
+          for (int k = 0; k < TC_BK / TC_UK; ++k) {
+            const uint64_t adv = (uint64_t)((k * TC_UK * 2) >> 4);
+            mma_f16_pair(dacc, ahi + adv, bhi + adv, idesc, (kin | k) != 0);
+            mma_f16_pair(dacc, ahi + adv, blo + adv, idesc, 1u);
+            mma_f16_pair(dacc, alo + adv, bhi + adv, idesc, 1u);
+          }
+          mma_commit_pair(&empty[s]);
+          if (kin == TC_KC - 1 || q == tl.nkb - 1) {
+            mma_commit_pair(&acc_full[buf]);
+            ++c;
+          }
         }
-        mma_commit_pair(&empty[s]);
-        if (kin == TC_KC - 1 || i == nkb - 1) mma_commit_pair(&acc_full[buf]);
       }
     }
     __syncwarp();
@@ -478,62 +508,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     // columns [128*h, 128*h + 128), h = (w-2)/4; chunks are promoted into FP32 registers.
     const int lg = warp & 3;
     const int half = (warp - 2) >> 2;
-    const int row = mblk * 128 + lg * 32 + lane;
     const uint32_t acc_empty0 = map_to_rank(smem_u32(&acc_empty[0]), 0);
-    float acc[128];
+    int c = 0;  // running chunk counter
+    for (int t = cluster; t < ntiles; t += nclusters) {
+      const PairTile tl = pair_tile(p, t, npm, nn);
+      const int row = (tl.mblk0 + (int)rank) * 128 + lg * 32 + lane;
+      float acc[128];
 #pragma unroll
-    for (int i = 0; i < 128; ++i) acc[i] = 0.f;
-    const int nchunks = (nkb + TC_KC - 1) / TC_KC;
-    for (int c = 0; c < nchunks; ++c) {
-      const int buf = c & 1;
-      mbar_wait(&acc_full[buf], (c >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+      const int nchunks = (tl.nkb + TC_KC - 1) / TC_KC;
+      for (int cc0 = 0; cc0 < nchunks; ++cc0, ++c) {
+        const int buf = c & 1;
+        mbar_wait(&acc_full[buf], (c >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-      for (int cc = 0; cc < 128; cc += 16) {
-        uint32_t v[16];
-        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * TC_BN + half * 128 + cc);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int cc = 0; cc < 128; cc += 16) {
+          uint32_t v[16];
+          const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * TC_BN + half * 128 + cc);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[cc + i] += __uint_as_float(v[i]);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(acc_empty0 + (uint32_t)(buf * sizeof(uint64_t)));
-    }
-    if (row < p.M) {
-      const float rs = inv_scale(p.amax[(int64_t)z * p.Mp + row]);
-      const float* bmx = p.bmax + (int64_t)bz * p.Np;
-      const int n0 = (nblk * TC_BN + half * 128) >> 1;
-      if (p.ksplit > 1) {
-        float2* W = p.ws + split * p.ws_split + ((int64_t)z * p.M + row) * p.N;
-#pragma unroll
-        for (int q = 0; q < 64; ++q) {
-          const int n = n0 + q;
-          if (n < p.N) {
-            const float sc = rs * inv_scale(bmx[n]);
-            W[n] = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
-          }
+          for (int i = 0; i < 16; ++i) acc[cc + i] += __uint_as_float(v[i]);
         }
-      } else {
-        const int b1 = (p.z0 + z) / p.nb2, b2 = (p.z0 + z) - b1 * p.nb2;
-        float2* Crow = p.C + b1 * p.sc1 + b2 * p.sc2 + (int64_t)row * p.cm;
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc_empty0 + (uint32_t)(buf * sizeof(uint64_t)));
+      }
+      if (row < p.M) {
+        const int z = tl.z, bz = p.b_batched ? z : 0;
+        const float rs = inv_scale(p.amax[(int64_t)z * p.Mp + row]);
+        const float* bmx = p.bmax + (int64_t)bz * p.Np;
+        const int n0 = (tl.nblk * TC_BN + half * 128) >> 1;
+        if (p.ksplit > 1) {
+          float2* W = p.ws + tl.split * p.ws_split + ((int64_t)z * p.M + row) * p.N;
 #pragma unroll
-        for (int q = 0; q < 64; ++q) {
-          const int n = n0 + q;
-          if (n < p.N) {
-            const float sc = rs * inv_scale(bmx[n]);
-            float2 val = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
-            if (p.accumulate) {
-              float2 o = Crow[n];
-              val.x += o.x;
-              val.y += o.y;
+          for (int q = 0; q < 64; ++q) {
+            const int n = n0 + q;
+            if (n < p.N) {
+              const float sc = rs * inv_scale(bmx[n]);
+              W[n] = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
             }
-            Crow[n] = val;
+          }
+        } else {
+          const int b1 = (p.z0 + z) / p.nb2, b2 = (p.z0 + z) - b1 * p.nb2;
+          float2* Crow = p.C + b1 * p.sc1 + b2 * p.sc2 + (int64_t)row * p.cm;
+#pragma unroll
+          for (int q = 0; q < 64; ++q) {
+            const int n = n0 + q;
+            if (n < p.N) {
+              const float sc = rs * inv_scale(bmx[n]);
+              float2 val = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
+              if (p.accumulate) {
+                float2 o = Crow[n];
+                val.x += o.x;
+                val.y += o.y;
+              }
+              Crow[n] = val;
+            }
           }
         }
       }
@@ -966,8 +1001,36 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
         mb_lo = make_map(bl.as<__half>() + (int64_t)z0 * Nrp * Krp, Krp, Nrp, nz, bbox);
       }
       if (pair) {
-        dim3 grid(Mp / TC_BM, Nrp / TC_BN, nz * ksplit);  // cluster (2,1,1) pairs M tiles
-        tc_gemm2_kernel<<<grid, TC_THREADS, SMEM2_BYTES, c.stream>>>(mah, mal, mb_hi, mb_lo, p);
+        // persistent CTA pairs over all (z, split, m pair, n) tiles
+        const int npm = Mp / (2 * TC_BM), nn = Nrp / TC_BN;
+        const int ntiles = nz * ksplit * npm * nn;
+        static int max_clusters = 0;
+        if (!max_clusters) {
+          // clusters that can be co-resident (a persistent grid larger than this would run
+          // its surplus clusters as a serial second wave)
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(148, 1, 1);
+          cfg.blockDim = dim3(TC_THREADS, 1, 1);
+          cfg.dynamicSmemBytes = SMEM2_BYTES;
+          cudaLaunchAttribute at;
+          at.id = cudaLaunchAttributeClusterDimension;
+          at.val.clusterDim.x = 2;
+          at.val.clusterDim.y = 1;
+          at.val.clusterDim.z = 1;
+          cfg.attrs = &at;
+          cfg.numAttrs = 1;
+          int n = 0;
+          if (cudaOccupancyMaxActiveClusters(&n, (void*)tc_gemm2_kernel, &cfg) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            n = 64;
+          }
+          max_clusters = std::min(n, 74);
+          if (getenv("TN_GEMM_LOG")) fprintf(stderr, "tc_gemm2: %d co-resident CTA pairs\n", max_clusters);
+        }
+        static const bool persist = !(getenv("TN_PERSIST") && std::atoi(getenv("TN_PERSIST")) == 0);
+        const int nclusters = persist ? std::min(ntiles, max_clusters) : ntiles;
+        tc_gemm2_kernel<<<2 * nclusters, TC_THREADS, SMEM2_BYTES, c.stream>>>(mah, mal, mb_hi, mb_lo, p, npm, nn,
+                                                                              ntiles);
       } else {
         dim3 grid(Nrp / TC_BN, Mp / TC_BM, nz * ksplit);
         tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mb_hi, mb_lo, p);

@@ -13,12 +13,16 @@ LIB.tn_debug_last_error.restype = C.c_char_p
 shapes = [(32768, 4096, 4096, 2), (16384, 2048, 1024, 4), (8192, 128, 4096, 8), (4096, 4096, 4096, 1),
           (128, 4096, 4096, 4), (300, 2048, 2048, 2)]
 modes = [int(x) for x in os.environ.get("MODES", "2,1").split(",")]
+# warm the clocks up (~1-2 s of GEMMs) before timing
+out = np.zeros(4)
+for _ in range(3):
+    LIB.tn_debug_gemm_bench(32768, 4096, 4096, 1, 2, 10, out.ctypes.data)
 for M, N, K, nb in shapes:
     for mode in modes:
         if mode == 1 and M * N * K * nb > 2 ** 36:
             continue
         out = np.zeros(4)
-        rc = LIB.tn_debug_gemm_bench(M, N, K, nb, mode, 5, out.ctypes.data)
+        rc = LIB.tn_debug_gemm_bench(M, N, K, nb, mode, int(os.environ.get('REPS', '10')), out.ctypes.data)
         assert rc == 0, LIB.tn_debug_last_error()
         ms, relerr = out[0], out[1]
         tf = 8.0 * M * N * K * nb / (ms * 1e-3) / 1e12
