@@ -636,15 +636,22 @@ struct PrepArgs {
   __half* lo;
 };
 
-__device__ __forceinline__ void load_tile(const PrepArgs& a, float2 (*tile)[33], int64_t* roff, int64_t* koff,
-                                          int r0, int k0, int zz) {
-  const int z = a.z0 + zz;
-  const int b1 = z / a.nb2, b2 = z - b1 * a.nb2;
-  const float2* base = a.X + b1 * a.s1 + b2 * a.s2;
-  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
-  if (t < 32) roff[t] = (r0 + t < a.R) ? view_off(a.vr, r0 + t) : -1;
-  else if (t < 64) koff[t - 32] = (k0 + t - 32 < a.K) ? view_off(a.vk, k0 + t - 32) : -1;
+// A CTA covers 32 rows x PK_K complex k (PK_K / 32 sub-tiles of 32 x 32 through shared
+// memory): the row offsets are computed once per CTA and the grid is PK_K / 32 times smaller
+// than one CTA per sub-tile.
+constexpr int PK_K = 128;
+
+__device__ __forceinline__ void prep_offsets(const PrepArgs& a, int64_t* roff, int64_t* koff, int r0, int k0) {
+  const int t = threadIdx.x;
+  if (t < PK_K) koff[t] = (k0 + t < a.K) ? view_off(a.vk, k0 + t) : -1;
+  else if (t < PK_K + 32) roff[t - PK_K] = (r0 + t - PK_K < a.R) ? view_off(a.vr, r0 + t - PK_K) : -1;
   __syncthreads();
+}
+
+__device__ __forceinline__ void load_sub(const PrepArgs& a, const float2* base, float2 (*tile)[33],
+                                         const int64_t* roff, const int64_t* koff) {
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+#pragma unroll
   for (int j = ty; j < 32; j += 8) {
     const int rr = a.k_fast ? j : tx, kk = a.k_fast ? tx : j;
     const int64_t ro = roff[rr], ko = koff[kk];
@@ -653,21 +660,43 @@ __device__ __forceinline__ void load_tile(const PrepArgs& a, float2 (*tile)[33],
     if (a.conj) v.y = -v.y;
     tile[rr][kk] = v;
   }
-  __syncthreads();
+}
+
+__device__ __forceinline__ const float2* prep_base(const PrepArgs& a, int zz) {
+  const int z = a.z0 + zz;
+  const int b1 = z / a.nb2, b2 = z - b1 * a.nb2;
+  return a.X + b1 * a.s1 + b2 * a.s2;
 }
 
 // Pass 1: max |component| of every row over K (atomicMax on the IEEE bits of a non-negative
 // float is order-independent, hence deterministic).
 __global__ void __launch_bounds__(256) rowmax_kernel(PrepArgs a) {
   __shared__ float2 tile[32][33];
-  __shared__ int64_t roff[32], koff[32];
-  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32, zz = blockIdx.z;
-  load_tile(a, tile, roff, koff, r0, k0, zz);
-  const int t = threadIdx.x;
+  __shared__ int64_t roff[32], koff[PK_K];
+  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * PK_K, zz = blockIdx.z;
+  prep_offsets(a, roff, koff, r0, k0);
+  const float2* base = prep_base(a, zz);
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  float m = 0.f;  // thread (ty, tx): row tx... reduced below
+  __shared__ float part[8][32];
+  for (int sub = 0; sub < PK_K / 32 && k0 + sub * 32 < a.K; ++sub) {
+    load_sub(a, base, tile, roff, koff + sub * 32);
+    __syncthreads();
+    // warp ty scans 4 k columns of every row tx
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 v = tile[tx][ty * 4 + q];
+      m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+    __syncthreads();
+  }
+  part[ty][tx] = m;
+  __syncthreads();
   if (t < 32 && r0 + t < a.R) {
-    float m = 0.f;
-    for (int k = 0; k < 32; ++k) m = fmaxf(m, fmaxf(fabsf(tile[t][k].x), fabsf(tile[t][k].y)));
-    if (m > 0.f) atomicMax(reinterpret_cast<unsigned int*>(a.mx + (int64_t)zz * a.Rp + r0 + t), __float_as_uint(m));
+    float mm = part[0][t];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) mm = fmaxf(mm, part[q][t]);
+    if (mm > 0.f) atomicMax(reinterpret_cast<unsigned int*>(a.mx + (int64_t)zz * a.Rp + r0 + t), __float_as_uint(mm));
   }
 }
 
@@ -676,64 +705,72 @@ __device__ __forceinline__ void split16(float x, __half& h, __half& l) {
   l = __float2half_rn(x - __half2float(h));
 }
 
+__device__ __forceinline__ void split16x2(float x, float y, __half2& h, __half2& l) {
+  __half hx, lx, hy, ly;
+  split16(x, hx, lx);
+  split16(y, hy, ly);
+  h = __halves2half2(hx, hy);
+  l = __halves2half2(lx, ly);
+}
+
 // Pass 2: scaled FP16 hi/lo planes. KIND 0: A planes [z][Rrows][Krp], element (r, 2k+c) =
 // (Re, Im)[c]. KIND 1: B_r^T planes [z][Rrows][Krp], rows 2r = (Re b, -Im b), 2r+1 = (Im b, Re b).
+// Each thread converts one complex element per row and stores half2 pairs (128 B per warp).
 template <int KIND>
 __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
   __shared__ float2 tile[32][33];
-  __shared__ int64_t roff[32], koff[32];
+  __shared__ int64_t roff[32], koff[PK_K];
   __shared__ float scl[32];
-  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32, zz = blockIdx.z;
+  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * PK_K, zz = blockIdx.z;
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
-  if (t < 32) {
-    const float m = (r0 + t < a.R) ? a.mx[(int64_t)zz * a.Rp + r0 + t] : 0.f;
-    scl[t] = 1.f;
-    if (m > 0.f) scl[t] = ldexpf(1.f, -scale_exp(m));
+  if (t >= 224) {
+    const int i = t - 224;
+    const float m = (r0 + i < a.R) ? a.mx[(int64_t)zz * a.Rp + r0 + i] : 0.f;
+    scl[i] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
   }
-  load_tile(a, tile, roff, koff, r0, k0, zz);
+  prep_offsets(a, roff, koff, r0, k0);
+  const float2* base = prep_base(a, zz);
   const int64_t plane = (int64_t)a.Rrows * a.Krp;
-  if (KIND == 0) {
-    for (int j = ty; j < 32; j += 8) {
-      const int r = r0 + j;
-      if (r >= a.Rrows) continue;
-      __half* hrow = a.hi + zz * plane + (int64_t)r * a.Krp;
-      __half* lrow = a.lo + zz * plane + (int64_t)r * a.Krp;
-      const float s = scl[j];
+  __half2* hi = reinterpret_cast<__half2*>(a.hi + zz * plane);
+  __half2* lo = reinterpret_cast<__half2*>(a.lo + zz * plane);
+  const int kp = a.Krp >> 1;  // half2 per plane row
+  for (int sub = 0; sub < PK_K / 32; ++sub) {
+    const int kb = k0 + sub * 32;
+    if (2 * kb >= a.Krp) break;
+    load_sub(a, base, tile, roff, koff + sub * 32);
+    __syncthreads();
+    const int kc = kb + tx;  // complex k of this thread
+    if (2 * kc < a.Krp) {
+      if (KIND == 0) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int kr2 = tx + 32 * h;  // 0..63 real columns of this tile
-        const int kr = 2 * k0 + kr2;
-        if (kr >= a.Krp) continue;
-        const float2 v = tile[j][kr2 >> 1];
-        const float x = ((kr2 & 1) ? v.y : v.x) * s;
-        __half hv, lv;
-        split16(x, hv, lv);
-        hrow[kr] = hv;
-        lrow[kr] = lv;
+        for (int j = ty; j < 32; j += 8) {
+          const int r = r0 + j;
+          if (r >= a.Rrows) continue;
+          const float2 v = tile[j][tx];
+          const float sc = scl[j];
+          __half2 h, l;
+          split16x2(v.x * sc, v.y * sc, h, l);
+          hi[(int64_t)r * kp + kc] = h;
+          lo[(int64_t)r * kp + kc] = l;
+        }
+      } else {
+#pragma unroll
+        for (int j = ty; j < 32; j += 8) {
+          const int row = 2 * (r0 + j);
+          if (row >= a.Rrows) continue;
+          const float2 b = tile[j][tx];
+          const float sc = scl[j];
+          __half2 h, l;
+          split16x2(b.x * sc, -b.y * sc, h, l);
+          hi[(int64_t)row * kp + kc] = h;
+          lo[(int64_t)row * kp + kc] = l;
+          split16x2(b.y * sc, b.x * sc, h, l);
+          hi[(int64_t)(row + 1) * kp + kc] = h;
+          lo[(int64_t)(row + 1) * kp + kc] = l;
+        }
       }
     }
-  } else {
-    for (int j = ty; j < 64; j += 8) {  // 64 plane rows = 32 complex columns of B
-      const int rr = j >> 1, par = j & 1;
-      const int row = 2 * r0 + j;
-      if (row >= a.Rrows) continue;
-      __half* hrow = a.hi + zz * plane + (int64_t)row * a.Krp;
-      __half* lrow = a.lo + zz * plane + (int64_t)row * a.Krp;
-      const float s = scl[rr];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int kr2 = tx + 32 * h;
-        const int kr = 2 * k0 + kr2;
-        if (kr >= a.Krp) continue;
-        const float2 b = tile[rr][kr2 >> 1];
-        const int sel = (par << 1) | (kr2 & 1);
-        const float x = (sel == 0 ? b.x : (sel == 1 ? -b.y : (sel == 2 ? b.y : b.x))) * s;
-        __half hv, lv;
-        split16(x, hv, lv);
-        hrow[kr] = hv;
-        lrow[kr] = lv;
-      }
-    }
+    __syncthreads();
   }
 }
 
@@ -906,10 +943,10 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     a.Rp = Np;
     a.hi = bh.as<__half>();
     a.lo = bl.as<__half>();
-    dim3 gmax(ceil_div(g.K, 32), ceil_div(g.N, 32), nzb);
+    dim3 gmax(ceil_div(g.K, PK_K), ceil_div(g.N, 32), nzb);
     rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
-    dim3 grid(ceil_div(Krp / 2, 32), Nrp / 64, nzb);
+    dim3 grid(ceil_div(Krp / 2, PK_K), Nrp / 64, nzb);
     prep_tiled_kernel<1><<<grid, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
   }
@@ -961,10 +998,10 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       a.hi = ah.as<__half>();
       a.lo = al.as<__half>();
       TN_CUDA(cudaMemsetAsync(amx.p, 0, (size_t)nz * Mp * sizeof(float), c.stream));
-      dim3 gmax(ceil_div(g.K, 32), ceil_div(g.M, 32), nz);
+      dim3 gmax(ceil_div(g.K, PK_K), ceil_div(g.M, 32), nz);
       rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
       TN_LAUNCHED();
-      dim3 grid(ceil_div(Krp / 2, 32), Mp / 32, nz);
+      dim3 grid(ceil_div(Krp / 2, PK_K), Mp / 32, nz);
       prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
       TN_LAUNCHED();
     }
