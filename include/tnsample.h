@@ -107,9 +107,35 @@ int tn_amplitude(tn_state* st, const uint8_t* bits, int64_t n, int32_t chi_env, 
 /* ln <psi|psi> ~ ln <M_{2->1}, T_1> for the current row order and chi_env (R12). */
 int tn_log_norm(tn_state* st, int32_t chi_env, double* out_lognorm);
 
+/* Sample certification. For n samples bits[k][v]
+ * with their sampled log-probabilities logq[k] = ln q(x_k) (from tn_sample), computes
+ * out_logp[k] = ln p(x_k) = 2 ln|<x_k|psi>| by a separate boundary-MPS contraction at bond
+ * chi_env_verify (the paper's verification rank, 2 chi by default, P:130 / R15) over the
+ * state's current row order, and the statistics of the importance weights w_k = p_k / q_k:
+ *   log_norm_estimate  ln( (1/n) sum_k w_k ): the unbiased estimator E_q[p/q] = <psi|psi>
+ *                      (P:116-121), evaluated with a log-sum-exp;
+ *   norm_rel_stderr    standard error of (1/n) sum_k w_k divided by that mean (0 if n == 1);
+ *   kld                (1/n) sum_k (ln q_k - ln p_k + ln Z), the sample KLD of Eq. (kld)
+ *                       with p normalised by Z (R12): ln Z = log_z if finite,
+ *                      else ln Z = log_norm_estimate;
+ *   ess                (sum w)^2 / sum w^2, the effective sample size of the weights.
+ * Samples with logq or logp = -inf/NaN are excluded from the statistics and counted in
+ * n_excluded. Host arrays; out_logp may be NULL. Errors: TN_E_ARG (NULL, n <= 0, bits not
+ * 0/1), TN_E_ROWS (no row order prepared), TN_E_CUDA. */
+typedef struct {
+  double log_norm_estimate;
+  double norm_rel_stderr;
+  double kld;
+  double ess;
+  int64_t n_used;
+  int64_t n_excluded;
+} tn_cert_stats;
+int tn_certify(tn_state* st, const uint8_t* bits, const double* logq, int64_t n, int32_t chi_env_verify,
+               double log_z, double* out_logp, tn_cert_stats* out);
+
 /* Options (SURVEY 5 "Config / flags"): "fit_half_sweeps" (nh, default 2, R5), "init_seed"
  * (default 0x2507114240, R4), "gemm" (0 = auto, 1 = force SIMT FP32, 2 = force tcgen05
- * TF32x3), "max_batch" (0 = auto from free device memory). Changing an option invalidates
+ * FP16x3), "max_batch" (0 = auto from free device memory). Changing an option invalidates
  * cached environments. Unknown name -> TN_E_ARG. */
 int tn_set_option(tn_state* st, const char* name, int64_t value);
 

@@ -17,13 +17,19 @@ TN_OK = 0
 ERRORS = {-1: "TN_E_ARG", -2: "TN_E_GRAPH", -3: "TN_E_ROWS", -4: "TN_E_NOMEM", -5: "TN_E_CUDA",
           -6: "TN_E_NCCL", -7: "TN_E_NUMERIC"}
 EXPORTS = ["tn_load_state", "tn_prepare", "tn_sample", "tn_sample_ex", "tn_sample_dev", "tn_amplitude",
-           "tn_log_norm", "tn_set_option", "tn_get_stats", "tn_free_state", "tn_last_error"]
+           "tn_log_norm", "tn_certify", "tn_set_option", "tn_get_stats", "tn_free_state", "tn_last_error"]
 
 
 class TNError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"{ERRORS.get(code, code)}: {msg}")
         self.code = code
+
+
+class CertStats(C.Structure):
+    """tn_cert_stats (include/tnsample.h)."""
+    _fields_ = [("log_norm_estimate", C.c_double), ("norm_rel_stderr", C.c_double), ("kld", C.c_double),
+                ("ess", C.c_double), ("n_used", C.c_int64), ("n_excluded", C.c_int64)]
 
 
 class _Graph(C.Structure):
@@ -44,6 +50,7 @@ def load_library(path: str = LIB_PATH):
     lib.tn_sample_dev.argtypes = [P, i32p, i32p, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P]
     lib.tn_amplitude.argtypes = [P, P, C.c_int64, C.c_int32, P, P]
     lib.tn_log_norm.argtypes = [P, C.c_int32, C.POINTER(C.c_double)]
+    lib.tn_certify.argtypes = [P, P, P, C.c_int64, C.c_int32, C.c_double, P, C.POINTER(CertStats)]
     lib.tn_set_option.argtypes = [P, C.c_char_p, C.c_int64]
     lib.tn_get_stats.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
     lib.tn_free_state.argtypes = [P]
@@ -155,6 +162,17 @@ class TNState:
         out = C.c_double()
         _check(lib().tn_log_norm(self._h, int(chi_env), C.byref(out)))
         return out.value
+
+    def certify(self, bits, logq, chi_env_verify: int, log_z: float = float("nan")):
+        """ln p(x) of every sample and the weight statistics of tn_certify (NEXT-1)."""
+        b = np.ascontiguousarray(bits, dtype=np.uint8)
+        q = np.ascontiguousarray(logq, dtype=np.float64)
+        n = b.shape[0]
+        lp = np.zeros(n)
+        st = CertStats()
+        _check(lib().tn_certify(self._h, _ptr(b), _ptr(q), n, int(chi_env_verify), float(log_z), _ptr(lp),
+                                C.byref(st)))
+        return lp, {k: getattr(st, k) for k, _ in CertStats._fields_}
 
     def stats(self):
         n = C.c_int64()

@@ -323,3 +323,86 @@ int64_t count_nonfinite(Ctx& c, const float2* p, int64_t n) {
   return (int64_t)h;
 }
 }  // namespace tn
+
+// ---- sample certification statistics (tn_certify). One CTA, FP64.
+namespace tn {
+namespace {
+__global__ void __launch_bounds__(1024) cert_kernel(const double* __restrict__ lq, const double* __restrict__ lp,
+                                                    int64_t n, double log_z, double* __restrict__ out) {
+  __shared__ double red[32];
+  __shared__ double s_bc;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  auto block_sum = [&](double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+      double x = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) s_bc = x;
+    }
+    __syncthreads();
+    double r = s_bc;
+    __syncthreads();
+    return r;
+  };
+  auto block_max = [&](double v) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+      double x = lane < (int)(blockDim.x >> 5) ? red[lane] : -INFINITY;
+      for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+      if (lane == 0) s_bc = x;
+    }
+    __syncthreads();
+    double r = s_bc;
+    __syncthreads();
+    return r;
+  };
+  double mx = -INFINITY, cnt = 0, dsum = 0;
+  for (int64_t k = t; k < n; k += blockDim.x) {
+    const double d = lp[k] - lq[k];
+    if (isfinite(d)) {
+      mx = fmax(mx, d);
+      cnt += 1;
+      dsum += -d;
+    }
+  }
+  mx = block_max(mx);
+  cnt = block_sum(cnt);
+  dsum = block_sum(dsum);
+  double s1 = 0, s2 = 0;
+  for (int64_t k = t; k < n; k += blockDim.x) {
+    const double d = lp[k] - lq[k];
+    if (isfinite(d)) {
+      const double e = exp(d - mx);
+      s1 += e;
+      s2 += e * e;
+    }
+  }
+  s1 = block_sum(s1);
+  s2 = block_sum(s2);
+  if (t == 0) {
+    const double mean = s1 / cnt;  // in units of e^mx
+    const double lne = mx + log(mean);
+    double rel = 0;
+    if (cnt > 1) {
+      const double var = fmax(0.0, (s2 / cnt - mean * mean) * cnt / (cnt - 1));
+      rel = sqrt(var / cnt) / mean;
+    }
+    const double lz = isfinite(log_z) ? log_z : lne;
+    out[0] = cnt > 0 ? lne : NAN;
+    out[1] = cnt > 0 ? rel : NAN;
+    out[2] = cnt > 0 ? dsum / cnt + lz : NAN;
+    out[3] = cnt > 0 ? s1 * s1 / s2 : 0;
+    out[4] = cnt;
+    out[5] = (double)n - cnt;
+  }
+}
+}  // namespace
+void cert_stats(Ctx& c, const double* logq, const double* logp, int64_t n, double log_z, double* out) {
+  cert_kernel<<<1, 1024, 0, c.stream>>>(logq, logp, n, log_z, out);
+  TN_LAUNCHED();
+}
+}  // namespace tn

@@ -8,6 +8,8 @@ namespace tn {
 void hash_init(Ctx& c, Tensor& o, int nb, uint64_t seed, int tag, int b1, int k);
 
 // Per-sample Frobenius norm: t <- t / ||t||, logn[b] (+)= ln ||t|| when logn != nullptr.
+// tn_certify statistics: out[0..5] = ln mean(p/q), rel. stderr, KLD, ESS, n used, n excluded
+void cert_stats(Ctx& c, const double* logq, const double* logp, int64_t n, double log_z, double* out);
 int64_t count_nonfinite(Ctx& c, const float2* p, int64_t n);  // debugging (synchronises)
 void normalize(Ctx& c, Tensor& t, int nb, double* logn, bool accumulate_log);
 

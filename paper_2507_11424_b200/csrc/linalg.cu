@@ -353,10 +353,9 @@ __device__ __forceinline__ float2 mv_ld(const MatView& V, int64_t b, int64_t i, 
 // part[b][sp][i][j] = sum over rows r of split sp of conj(Y(r, i)) X(r, j); herm: skip tiles
 // strictly above the diagonal (only the lower triangle i >= j is consumed).
 __global__ void __launch_bounds__(256) gram64_kernel(MatView Y, MatView X, int m, int splits, int herm,
-                                                     const int* __restrict__ rank, int skip_full,
-                                                     double2* __restrict__ part) {
+                                                     const int* __restrict__ active, double2* __restrict__ part) {
   const int b = blockIdx.z / splits, sp = blockIdx.z - b * splits;
-  if (rank && skip_full && rank[b] >= X.n) return;
+  if (active && !active[b]) return;
   const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
   if (herm && i0 + GT <= j0) return;
   __shared__ double2 sy[GK][GT];
@@ -417,11 +416,15 @@ __global__ void __launch_bounds__(256) gram64_kernel(MatView Y, MatView X, int m
 }
 
 // O(i, j) = sum_k X(i, k) W[b][k][j]  (X FP32 view, W FP64 [n][n], O FP32 view)
+// active: per-matrix switch (NULL = all); sel: per-matrix output choice (NULL or sel[b] != 0 ->
+// O, else O2).
 __global__ void __launch_bounds__(256) apply64v_kernel(MatView X, const double2* __restrict__ Wall, MatView O,
-                                                       const int* __restrict__ rank, int skip_full) {
+                                                       const int* __restrict__ active, const int* __restrict__ sel,
+                                                       MatView O2) {
   const int b = blockIdx.z;
   const int m = X.m, n = X.n;
-  if (rank && skip_full && rank[b] >= n) return;
+  if (active && !active[b]) return;
+  if (sel && !sel[b]) O = O2;
   __shared__ double2 sa[GT][GK + 1];
   __shared__ double2 sw[GK][GT];
   const int i0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
@@ -489,15 +492,20 @@ __device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; } 
 // diagonal with rank detection (diag <= tol * max initial diag stops; rank < n matrices get
 // no W -- the completion path handles them). Without PIVOT, tiny pivots are clamped and
 // flagged in *bad. Everything lives in shared memory (packed lower triangle in FP64).
+// PIVOT also writes deficient[b] = (rank < n) and need2[b] = 1 when a second CholeskyQR
+// pass is needed: rank deficiency, or a pivot ratio l_11 / l_nn > 1e3 (an estimate of the
+// condition number; below it the single pass, with its Gram exact in FP64 for FP32 data,
+// is orthogonal to ~kappa^2 1e-16 < FP32 rounding).
 template <bool PIVOT>
 __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __restrict__ part, int splits, int n,
                                                                double tol, double2* __restrict__ Wall,
                                                                int* __restrict__ perm_all, int* __restrict__ rank_all,
                                                                double* __restrict__ dmax_all, int* __restrict__ bad,
-                                                               const int* __restrict__ rank_in, int skip_full) {
+                                                               const int* __restrict__ active,
+                                                               int* __restrict__ deficient, int* __restrict__ need2) {
   extern __shared__ double2 chs[];
   const int b = blockIdx.x;
-  if (rank_in && skip_full && rank_in[b] >= n) return;
+  if (active && !active[b]) return;
   double2* S = chs;                                       // packed lower, original indices
   double2* Y = S + CH_MAXN * (CH_MAXN + 1) / 2;           // [32 warps][CH_MAXN]
   double2* lv = Y + (CH_THREADS / 32) * CH_MAXN;          // [CH_MAXN]
@@ -624,6 +632,13 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
   if (PIVOT && t == 0) {
     rank_all[b] = rank;
     dmax_all[b] = d0;
+    deficient[b] = rank < n ? 1 : 0;
+    int nd = 1;
+    if (rank == n && n > 0) {
+      const double l0 = S[pk(perm[0], perm[0])].x, l1 = S[pk(perm[n - 1], perm[n - 1])].x;
+      nd = (l1 > 0 && l0 <= 1e3 * l1) ? 0 : 1;
+    }
+    need2[b] = nd;
   }
   if (PIVOT) {
     for (int i = t; i < n; i += CH_THREADS) perm_all[(int64_t)b * n + i] = perm[i];
@@ -703,13 +718,13 @@ static int gram_splits(int m, int nI, int nJ) {
   return std::max(1, std::min({want, std::max(1, m / 128), 64}));
 }
 
-static void gram(Ctx& c, const MatView& Y, const MatView& X, int m, int nb, bool herm, const int* rank,
-                 int skip_full, DevBuf& part, int& splits) {
+static void gram(Ctx& c, const MatView& Y, const MatView& X, int m, int nb, bool herm, const int* active,
+                 DevBuf& part, int& splits) {
   splits = gram_splits(m, Y.n, X.n);
   size_t need = (size_t)nb * splits * Y.n * X.n * sizeof(double2);
   if (part.bytes < need) part.alloc(need, c.stream);
   dim3 grid(ceil_div(X.n, GT), ceil_div(Y.n, GT), (unsigned)(nb * splits));
-  gram64_kernel<<<grid, 256, 0, c.stream>>>(Y, X, m, splits, herm ? 1 : 0, rank, skip_full, part.as<double2>());
+  gram64_kernel<<<grid, 256, 0, c.stream>>>(Y, X, m, splits, herm ? 1 : 0, active, part.as<double2>());
   TN_LAUNCHED();
 }
 
@@ -721,26 +736,32 @@ static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, 
     TN_CUDA(cudaFuncSetAttribute(chol_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CH_SMEM));
     attr = true;
   }
+  static const double tol = getenv("TN_ORTH_TOL") ? atof(getenv("TN_ORTH_TOL")) : 1e-13;
+  static const bool always2 = getenv_flag("TN_ORTH_ALWAYS2");
   const size_t nn = (size_t)n * n * nb;
   DevBuf part, W(nn * sizeof(double2), c.stream);
   DevBuf perm((size_t)n * nb * sizeof(int), c.stream), rank((size_t)nb * sizeof(int), c.stream);
   DevBuf dmax((size_t)nb * sizeof(double), c.stream), bad(sizeof(int), c.stream);
+  DevBuf flags((size_t)2 * nb * sizeof(int), c.stream);
+  int* deficient = flags.as<int>();
+  int* need2 = deficient + nb;
   DevBuf Q1((size_t)m * n * nb * sizeof(float2), c.stream);
   TN_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
   MatView Q1v{Q1.as<float2>(), (int64_t)m * n, n, 1, false, m, n};
   const dim3 agrid(ceil_div(n, GT), ceil_div(m, GT), nb);
   int splits = 1;
-  // pass 1: G = X^H X, pivoted Cholesky (rank detection); full rank: Q1 = X P L^-H
-  gram(c, X, X, m, nb, true, nullptr, 0, part, splits);
-  static const double tol = getenv("TN_ORTH_TOL") ? atof(getenv("TN_ORTH_TOL")) : 1e-13;
-  chol_smem_kernel<true><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, tol,
-                                                                W.as<double2>(), perm.as<int>(), rank.as<int>(),
-                                                                dmax.as<double>(), bad.as<int>(), nullptr, 0);
+  // pass 1: G = X^H X, pivoted Cholesky (rank detection, condition estimate); full rank:
+  // Q1 = X P L^-H, written straight to Q when no second pass is needed
+  gram(c, X, X, m, nb, true, nullptr, part, splits);
+  chol_smem_kernel<true><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, tol, W.as<double2>(),
+                                                                perm.as<int>(), rank.as<int>(), dmax.as<double>(),
+                                                                bad.as<int>(), nullptr, deficient, need2);
   TN_LAUNCHED();
-  apply64v_kernel<<<agrid, 256, 0, c.stream>>>(X, W.as<double2>(), Q1v, nullptr, 0);
+  if (always2) TN_CUDA(cudaMemsetAsync(need2, 0xFF, sizeof(int) * nb, c.stream));  // (-1: every matrix)
+  apply64v_kernel<<<agrid, 256, 0, c.stream>>>(X, W.as<double2>(), Q1v, nullptr, need2, Q);
   TN_LAUNCHED();
-  // rank-deficient matrices only (every kernel returns at once for full-rank ones):
-  // X' = [X P(:, :r), Y] -> Cholesky -> Q1 = X' R'^-1
+  // rank-deficient matrices only (every kernel returns at once for the others):
+  // X' = [X P(:, :r), Y] -> Cholesky -> Q1 = X' R'^-1 (need2 is set for them)
   {
     DevBuf Ap((size_t)m * n * nb * sizeof(float2), c.stream);
     int64_t tot = (int64_t)m * n * nb;
@@ -749,24 +770,24 @@ static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, 
                                                dmax.as<double>(), nb);
     TN_LAUNCHED();
     MatView Av{Ap.as<float2>(), (int64_t)m * n, n, 1, false, m, n};
-    gram(c, Av, Av, m, nb, true, rank.as<int>(), 1, part, splits);
+    gram(c, Av, Av, m, nb, true, deficient, part, splits);
     chol_smem_kernel<false><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, 0.0,
-                                                                   W.as<double2>(), perm.as<int>(), rank.as<int>(),
-                                                                   dmax.as<double>(), bad.as<int>(), rank.as<int>(), 1);
+                                                                   W.as<double2>(), nullptr, nullptr, nullptr,
+                                                                   bad.as<int>(), deficient, nullptr, nullptr);
     TN_LAUNCHED();
-    apply64v_kernel<<<agrid, 256, 0, c.stream>>>(Av, W.as<double2>(), Q1v, rank.as<int>(), 1);
+    apply64v_kernel<<<agrid, 256, 0, c.stream>>>(Av, W.as<double2>(), Q1v, deficient, nullptr, Q1v);
     TN_LAUNCHED();
   }
-  // pass 2 (re-orthogonalisation): G2 = Q1^H Q1 -> Q = Q1 R2^-1
-  gram(c, Q1v, Q1v, m, nb, true, nullptr, 0, part, splits);
-  chol_smem_kernel<false><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, 0.0,
-                                                                 W.as<double2>(), perm.as<int>(), nullptr,
-                                                                 nullptr, bad.as<int>(), nullptr, 0);
+  // pass 2 (re-orthogonalisation) where needed: G2 = Q1^H Q1 -> Q = Q1 R2^-1
+  gram(c, Q1v, Q1v, m, nb, true, need2, part, splits);
+  chol_smem_kernel<false><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, 0.0, W.as<double2>(),
+                                                                 nullptr, nullptr, nullptr, bad.as<int>(), need2,
+                                                                 nullptr, nullptr);
   TN_LAUNCHED();
-  apply64v_kernel<<<agrid, 256, 0, c.stream>>>(Q1v, W.as<double2>(), Q, nullptr, 0);
+  apply64v_kernel<<<agrid, 256, 0, c.stream>>>(Q1v, W.as<double2>(), Q, need2, nullptr, Q);
   TN_LAUNCHED();
   if (Cout) {
-    gram(c, Q, X, m, nb, false, nullptr, 0, part, splits);
+    gram(c, Q, X, m, nb, false, nullptr, part, splits);
     int64_t per = (int64_t)n * n;
     unsigned blocks = (unsigned)std::min<int64_t>((per * nb + 255) / 256, 4096);
     reduce_splits<<<blocks, 256, 0, c.stream>>>(part.as<double2>(), W.as<double2>(), splits, per, nb);

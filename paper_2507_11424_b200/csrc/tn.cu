@@ -732,6 +732,33 @@ int tn_log_norm(tn_state* st, int32_t chi_env, double* out_lognorm) {
   });
 }
 
+int tn_certify(tn_state* st, const uint8_t* bits, const double* logq, int64_t n, int32_t chi_env_verify,
+               double log_z, double* out_logp, tn_cert_stats* out) {
+  return guarded([&] {
+    if (!st || !bits || !logq || !out) throw Error(TN_E_ARG, "NULL argument");
+    if (n <= 0) throw Error(TN_E_ARG, "n must be > 0");
+    std::vector<double> la(n), ph(n), lp(n);
+    int rc = tn_amplitude(st, bits, n, chi_env_verify, la.data(), ph.data());
+    if (rc != TN_OK) throw Error(rc, g_err);
+    for (int64_t k = 0; k < n; ++k) lp[k] = 2.0 * la[k];
+    Ctx& c = st->ctx;
+    DevBuf dq(sizeof(double) * n, c.stream), dp(sizeof(double) * n, c.stream), ds(sizeof(double) * 8, c.stream);
+    TN_CUDA(cudaMemcpyAsync(dq.p, logq, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    TN_CUDA(cudaMemcpyAsync(dp.p, lp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    cert_stats(c, dq.as<double>(), dp.as<double>(), n, log_z, ds.as<double>());
+    double h[8];
+    TN_CUDA(cudaMemcpyAsync(h, ds.p, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+    TN_CUDA(cudaStreamSynchronize(c.stream));
+    out->log_norm_estimate = h[0];
+    out->norm_rel_stderr = h[1];
+    out->kld = h[2];
+    out->ess = h[3];
+    out->n_used = (int64_t)h[4];
+    out->n_excluded = (int64_t)h[5];
+    if (out_logp) std::copy(lp.begin(), lp.end(), out_logp);
+  });
+}
+
 int tn_get_stats(tn_state* st, int64_t* out_launches, double* out_precompute_s) {
   return guarded([&] {
     if (!st) throw Error(TN_E_ARG, "state is NULL");

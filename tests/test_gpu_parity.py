@@ -166,3 +166,28 @@ def test_batch_size_determinism():
     g.set_option("max_batch", 7)
     b2, l2, _, _ = g.sample(lat.rows, 16, u)
     assert (b1 == b2).all() and np.array_equal(l1, l2)
+
+
+def test_certify_matches_oracle_metrics():
+    """tn_certify (NEXT-1, P:114-128): ln p from the GPU amplitude path equals the statevector;
+    the weight statistics equal the oracle's metrics on the same (ln q, ln p)."""
+    from oracle import metrics
+    lat = L.square(3, 3)
+    st = S.vidal_like(lat, 2, seed=3, xi=2.0)
+    psi = SV.statevector(st)
+    u = S.uniforms(64, lat.n, 7)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 2, u)  # chi_env = 2 < exact: q != p
+    lz = math.log(np.vdot(psi, psi).real)
+    lp, stt = g.certify(bits, logq, 16, log_z=lz)
+    for k in range(len(u)):
+        idx = int("".join(map(str, bits[k])), 2)
+        assert abs(lp[k] - math.log(abs(psi[idx]) ** 2)) < 1e-4 * max(1.0, abs(lp[k]))
+    est, se = metrics.norm_estimate(logq, lp)
+    assert abs(stt["log_norm_estimate"] - math.log(est)) < 1e-9
+    assert abs(stt["norm_rel_stderr"] - se / est) < 1e-9
+    assert abs(stt["kld"] - metrics.kld(logq, lp - lz)) < 1e-9
+    r = np.exp(lp - logq)
+    assert abs(stt["ess"] - r.sum() ** 2 / (r ** 2).sum()) < 1e-6 * len(r)
+    assert stt["n_used"] == len(u) and stt["n_excluded"] == 0
+    # unbiasedness (P:116-121): the estimate is within a few standard errors of <psi|psi>
+    assert abs(math.exp(stt["log_norm_estimate"] - lz) - 1) < 5 * stt["norm_rel_stderr"] + 1e-6
