@@ -330,7 +330,9 @@ constexpr int T2_STAGES = 3;
 constexpr int A2_TILE = 128 * TC_BK * 2;                 // 16 KB per CTA
 constexpr int B2_TILE = 128 * TC_BK * 2;                 // 16 KB per CTA (half of the B tile)
 constexpr int STAGE2_BYTES = 2 * A2_TILE + 2 * B2_TILE;  // 64 KB
-constexpr int SMEM2_BYTES = T2_STAGES * STAGE2_BYTES + 1024 + 256;
+constexpr int EPI_Q = 8;                                 // complex columns per staged store step
+constexpr int EPI_STAGE_BYTES = 8 * 32 * (EPI_Q + 1) * 8;  // per-warp 32 x (8+1) float2 (8 warps)
+constexpr int SMEM2_BYTES = T2_STAGES * STAGE2_BYTES + EPI_STAGE_BYTES + 1024 + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -414,6 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   uint64_t* acc_full = empty + T2_STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float2* epi_stage = reinterpret_cast<float2*>(smem + T2_STAGES * STAGE2_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -538,38 +541,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(acc_empty0 + (uint32_t)(buf * sizeof(uint64_t)));
       }
-      if (row < p.M) {
+      // Coalesced output: each warp stages 32 rows x 8 complex columns in shared memory
+      // (padded rows), then writes 4 rows per store instruction (8 lanes x 8 B = 64 B each),
+      // instead of 32 scattered rows per instruction.
+      {
         const int z = tl.z, bz = p.b_batched ? z : 0;
-        const float rs = inv_scale(p.amax[(int64_t)z * p.Mp + row]);
+        const int row0 = (tl.mblk0 + (int)rank) * 128 + lg * 32;
+        const float rs = (row < p.M) ? inv_scale(p.amax[(int64_t)z * p.Mp + row]) : 0.f;
         const float* bmx = p.bmax + (int64_t)bz * p.Np;
         const int n0 = (tl.nblk * TC_BN + half * 128) >> 1;
+        float2* base;
+        int64_t ld;
+        bool acc_out = false;
         if (p.ksplit > 1) {
-          float2* W = p.ws + tl.split * p.ws_split + ((int64_t)z * p.M + row) * p.N;
-#pragma unroll
-          for (int q = 0; q < 64; ++q) {
-            const int n = n0 + q;
-            if (n < p.N) {
-              const float sc = rs * inv_scale(bmx[n]);
-              W[n] = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
-            }
-          }
+          base = p.ws + tl.split * p.ws_split + (int64_t)z * p.M * p.N;
+          ld = p.N;
         } else {
           const int b1 = (p.z0 + z) / p.nb2, b2 = (p.z0 + z) - b1 * p.nb2;
-          float2* Crow = p.C + b1 * p.sc1 + b2 * p.sc2 + (int64_t)row * p.cm;
+          base = p.C + b1 * p.sc1 + b2 * p.sc2;
+          ld = p.cm;
+          acc_out = p.accumulate != 0;
+        }
+        float2* stg = epi_stage + (warp - 2) * 32 * (EPI_Q + 1);
+        const int sub = lane >> 3, col = lane & 7;
 #pragma unroll
-          for (int q = 0; q < 64; ++q) {
-            const int n = n0 + q;
-            if (n < p.N) {
-              const float sc = rs * inv_scale(bmx[n]);
-              float2 val = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
-              if (p.accumulate) {
-                float2 o = Crow[n];
+        for (int q0 = 0; q0 < 64; q0 += EPI_Q) {
+#pragma unroll
+          for (int q = 0; q < EPI_Q; ++q) {
+            const int n = n0 + q0 + q;
+            const float sc = (n < p.N) ? rs * inv_scale(bmx[n]) : 0.f;
+            stg[lane * (EPI_Q + 1) + q] = make_float2(acc[2 * (q0 + q)] * sc, acc[2 * (q0 + q) + 1] * sc);
+          }
+          __syncwarp();
+          const int n = n0 + q0 + col;
+#pragma unroll 4
+          for (int r = 0; r < 32; r += 4) {
+            const int rr = r + sub, grow = row0 + rr;
+            if (grow < p.M && n < p.N) {
+              float2 val = stg[rr * (EPI_Q + 1) + col];
+              float2* dst = base + (int64_t)grow * ld + n;
+              if (acc_out) {
+                const float2 o = *dst;
                 val.x += o.x;
                 val.y += o.y;
               }
-              Crow[n] = val;
+              *dst = val;
             }
           }
+          __syncwarp();
         }
       }
     }
