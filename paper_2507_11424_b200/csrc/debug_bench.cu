@@ -108,3 +108,50 @@ extern "C" int tn_debug_row_cmacs(double* out, int n) {
   for (int i = 0; i < n && i < m; ++i) out[i] = tn::g_row_cmacs[i];
   return m;
 }
+
+#include "linalg.h"
+
+// Timing of one batched orthonormalisation (debug/benchmark only): nb random m x n matrices
+// (well conditioned), `reps` calls, average ms per call in out[0].
+extern "C" int tn_debug_orth_bench(int m, int n, int nb, int reps, int with_c, double* out) {
+  try {
+    Ctx c;
+    TN_CUDA(cudaStreamCreate(&c.stream));
+    {
+      int dev = 0;
+      cudaMemPool_t pool;
+      TN_CUDA(cudaGetDevice(&dev));
+      TN_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t thr = UINT64_MAX;
+      TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    size_t sz = (size_t)m * n * nb;
+    DevBuf dx(sz * sizeof(float2), c.stream), dq(sz * sizeof(float2), c.stream),
+        dc((size_t)n * n * nb * sizeof(float2), c.stream);
+    fill_hash<<<1184, 256, 0, c.stream>>>(dx.as<float2>(), (int64_t)sz, 7);
+    MatView xv{dx.as<float2>(), (int64_t)m * n, n, 1, false, m, n};
+    MatView qv{dq.as<float2>(), (int64_t)m * n, n, 1, false, m, n};
+    orthonormalize(c, xv, qv, with_c ? dc.as<float2>() : nullptr, nb);
+    cudaEvent_t e0, e1;
+    TN_CUDA(cudaEventCreate(&e0));
+    TN_CUDA(cudaEventCreate(&e1));
+    TN_CUDA(cudaEventRecord(e0, c.stream));
+    for (int r = 0; r < reps; ++r) orthonormalize(c, xv, qv, with_c ? dc.as<float2>() : nullptr, nb);
+    TN_CUDA(cudaEventRecord(e1, c.stream));
+    TN_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    TN_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    out[0] = t / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    dx.release();
+    dq.release();
+    dc.release();
+    TN_CUDA(cudaStreamSynchronize(c.stream));
+    cudaStreamDestroy(c.stream);
+    return 0;
+  } catch (const std::exception& e) {
+    fprintf(stderr, "%s\n", e.what());
+    return -1;
+  }
+}

@@ -251,6 +251,24 @@ std::vector<int> fit_bonds(const DStrip& s, int R) {
   return std::vector<int>(D.begin(), D.end());
 }
 
+// Profiling aid only (TN_FAKE_ENVS): the output sites of the fit with their structural shapes,
+// filled with the hash initial guess and normalised, without fitting.
+FitResult fake_fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed) {
+  FitResult res;
+  std::vector<int> cols;
+  for (int j = 0; j < s.W; ++j)
+    if (s.out[j]) cols.push_back(j);
+  std::vector<int> D = fit_bonds(s, R);
+  for (size_t k = 0; k < cols.size(); ++k) {
+    Tensor o = new_tensor_n(c, o_shape(s, cols[k], D[k], D[k + 1]), 1);
+    o.bstride = 0;
+    hash_init(c, o, 1, seed, tag, b1, (int)k);
+    normalize(c, o, 1, nullptr, false);
+    res.sites.push_back(o);
+  }
+  return res;
+}
+
 FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, int nh, double* logn,
               bool accumulate) {
   Ops ops{c, s};

@@ -36,6 +36,8 @@ std::vector<int> fit_bonds(const DStrip& s, int R);
 // TN_NAN_CHECK debugging aid (synchronises; no-op unless the variable is set)
 void nan_check(Ctx& c, const char* what, const Tensor& t, int nb);
 
+FitResult fake_fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed);  // profiling only
+
 FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, int nh, double* logn,
               bool accumulate);
 

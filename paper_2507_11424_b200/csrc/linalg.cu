@@ -81,6 +81,34 @@ __global__ void reduce_splits(const double2* __restrict__ part, double2* __restr
   }
 }
 
+// G[b] = sum over splits of the Gram partials (fixed order, 4 independent partial sums so the
+// loads overlap); herm: lower triangle only; inactive matrices skipped.
+__global__ void reduce_gram_kernel(const double2* __restrict__ part, double2* __restrict__ out, int splits, int nI,
+                                   int nJ, int nb, int herm, const int* __restrict__ active) {
+  const int64_t per = (int64_t)nI * nJ, tot = per * nb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / per, r = e - b * per;
+    if (active && !active[b]) continue;
+    if (herm && (r % nJ) > (r / nJ)) continue;
+    const double2* p = part + b * splits * per + r;
+    double2 s0 = make_double2(0, 0), s1 = s0, s2 = s0, s3 = s0;
+    int k = 0;
+    for (; k + 4 <= splits; k += 4) {
+      const double2 v0 = p[(k + 0) * per], v1 = p[(k + 1) * per], v2 = p[(k + 2) * per], v3 = p[(k + 3) * per];
+      s0.x += v0.x; s0.y += v0.y;
+      s1.x += v1.x; s1.y += v1.y;
+      s2.x += v2.x; s2.y += v2.y;
+      s3.x += v3.x; s3.y += v3.y;
+    }
+    for (; k < splits; ++k) {
+      const double2 v = p[k * per];
+      s0.x += v.x;
+      s0.y += v.y;
+    }
+    out[e] = make_double2((s0.x + s1.x) + (s2.x + s3.x), (s0.y + s1.y) + (s2.y + s3.y));
+  }
+}
+
 // ---- pivoted Cholesky (rank detection). One CTA per matrix; G (n x n, full Hermitian)
 // is overwritten. Outputs perm[b][n], rank[b], dmax[b] (largest initial diagonal).
 __global__ void __launch_bounds__(512) pivchol_kernel(double2* __restrict__ Gall, int n, double tol,
@@ -718,13 +746,19 @@ static int gram_splits(int m, int nI, int nJ) {
   return std::max(1, std::min({want, std::max(1, m / 128), 64}));
 }
 
+// G[b] = Y^H X (FP64, [nb][nY][nX]; lower triangle only when herm) via split partials and a
+// parallel fixed-order reduction. The partials' buffer is reused across calls.
 static void gram(Ctx& c, const MatView& Y, const MatView& X, int m, int nb, bool herm, const int* active,
-                 DevBuf& part, int& splits) {
-  splits = gram_splits(m, Y.n, X.n);
+                 DevBuf& part, double2* G) {
+  const int splits = gram_splits(m, Y.n, X.n);
   size_t need = (size_t)nb * splits * Y.n * X.n * sizeof(double2);
   if (part.bytes < need) part.alloc(need, c.stream);
   dim3 grid(ceil_div(X.n, GT), ceil_div(Y.n, GT), (unsigned)(nb * splits));
   gram64_kernel<<<grid, 256, 0, c.stream>>>(Y, X, m, splits, herm ? 1 : 0, active, part.as<double2>());
+  TN_LAUNCHED();
+  const int64_t tot = (int64_t)nb * Y.n * X.n;
+  const unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+  reduce_gram_kernel<<<blocks, 256, 0, c.stream>>>(part.as<double2>(), G, splits, Y.n, X.n, nb, herm ? 1 : 0, active);
   TN_LAUNCHED();
 }
 
@@ -739,7 +773,7 @@ static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, 
   static const double tol = getenv("TN_ORTH_TOL") ? atof(getenv("TN_ORTH_TOL")) : 1e-13;
   static const bool always2 = getenv_flag("TN_ORTH_ALWAYS2");
   const size_t nn = (size_t)n * n * nb;
-  DevBuf part, W(nn * sizeof(double2), c.stream);
+  DevBuf part, W(nn * sizeof(double2), c.stream), Gm(nn * sizeof(double2), c.stream);
   DevBuf perm((size_t)n * nb * sizeof(int), c.stream), rank((size_t)nb * sizeof(int), c.stream);
   DevBuf dmax((size_t)nb * sizeof(double), c.stream), bad(sizeof(int), c.stream);
   DevBuf flags((size_t)2 * nb * sizeof(int), c.stream);
@@ -749,11 +783,10 @@ static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, 
   TN_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
   MatView Q1v{Q1.as<float2>(), (int64_t)m * n, n, 1, false, m, n};
   const dim3 agrid(ceil_div(n, GT), ceil_div(m, GT), nb);
-  int splits = 1;
   // pass 1: G = X^H X, pivoted Cholesky (rank detection, condition estimate); full rank:
   // Q1 = X P L^-H, written straight to Q when no second pass is needed
-  gram(c, X, X, m, nb, true, nullptr, part, splits);
-  chol_smem_kernel<true><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, tol, W.as<double2>(),
+  gram(c, X, X, m, nb, true, nullptr, part, Gm.as<double2>());
+  chol_smem_kernel<true><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(Gm.as<double2>(), 1, n, tol, W.as<double2>(),
                                                                 perm.as<int>(), rank.as<int>(), dmax.as<double>(),
                                                                 bad.as<int>(), nullptr, deficient, need2);
   TN_LAUNCHED();
@@ -770,8 +803,8 @@ static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, 
                                                dmax.as<double>(), nb);
     TN_LAUNCHED();
     MatView Av{Ap.as<float2>(), (int64_t)m * n, n, 1, false, m, n};
-    gram(c, Av, Av, m, nb, true, deficient, part, splits);
-    chol_smem_kernel<false><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, 0.0,
+    gram(c, Av, Av, m, nb, true, deficient, part, Gm.as<double2>());
+    chol_smem_kernel<false><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(Gm.as<double2>(), 1, n, 0.0,
                                                                    W.as<double2>(), nullptr, nullptr, nullptr,
                                                                    bad.as<int>(), deficient, nullptr, nullptr);
     TN_LAUNCHED();
@@ -779,21 +812,17 @@ static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, 
     TN_LAUNCHED();
   }
   // pass 2 (re-orthogonalisation) where needed: G2 = Q1^H Q1 -> Q = Q1 R2^-1
-  gram(c, Q1v, Q1v, m, nb, true, need2, part, splits);
-  chol_smem_kernel<false><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(part.as<double2>(), splits, n, 0.0, W.as<double2>(),
+  gram(c, Q1v, Q1v, m, nb, true, need2, part, Gm.as<double2>());
+  chol_smem_kernel<false><<<nb, CH_THREADS, CH_SMEM, c.stream>>>(Gm.as<double2>(), 1, n, 0.0, W.as<double2>(),
                                                                  nullptr, nullptr, nullptr, bad.as<int>(), need2,
                                                                  nullptr, nullptr);
   TN_LAUNCHED();
   apply64v_kernel<<<agrid, 256, 0, c.stream>>>(Q1v, W.as<double2>(), Q, need2, nullptr, Q);
   TN_LAUNCHED();
   if (Cout) {
-    gram(c, Q, X, m, nb, false, nullptr, part, splits);
-    int64_t per = (int64_t)n * n;
-    unsigned blocks = (unsigned)std::min<int64_t>((per * nb + 255) / 256, 4096);
-    reduce_splits<<<blocks, 256, 0, c.stream>>>(part.as<double2>(), W.as<double2>(), splits, per, nb);
-    TN_LAUNCHED();
+    gram(c, Q, X, m, nb, false, nullptr, part, Gm.as<double2>());
     unsigned b2 = (unsigned)std::min<int64_t>(((int64_t)nn + 255) / 256, 4096);
-    d2f_kernel<<<b2, 256, 0, c.stream>>>(W.as<double2>(), Cout, (int64_t)nn);
+    d2f_kernel<<<b2, 256, 0, c.stream>>>(Gm.as<double2>(), Cout, (int64_t)nn);
     TN_LAUNCHED();
   }
 }

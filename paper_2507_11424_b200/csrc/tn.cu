@@ -251,7 +251,11 @@ Envs& norm_envs(tn_state* st, Layout& L, int R) {
       s.mats.push_back(L.A[v]);
       s.out.push_back(has(L, v, 0));
     }
-    FitResult fr = fit(c, s, R, 2, b + 1, st->seed, st->nh, logd.as<double>() + (b - 1), false);
+    // TN_FAKE_ENVS=1 (profiling the per-sample path at full shapes only): structural shapes,
+    // hash values, no fit -- the samples drawn are meaningless.
+    static const bool fake = getenv("TN_FAKE_ENVS") && std::atoi(getenv("TN_FAKE_ENVS")) != 0;
+    FitResult fr = fake ? fake_fit(c, s, R, 2, b + 1, st->seed)
+                        : fit(c, s, R, 2, b + 1, st->seed, st->nh, logd.as<double>() + (b - 1), false);
     E.M[b - 1] = fr.sites;
   }
   TN_CUDA(cudaMemcpyAsync(E.logs.data(), logd.p, sizeof(double) * nbr, cudaMemcpyDeviceToHost, c.stream));

@@ -1,0 +1,14 @@
+"""Time batched orthonormalisation (debug entry point) at the fit's panel shapes."""
+import ctypes as C
+import os
+
+import numpy as np
+
+from paper_2507_11424_b200 import _lib
+
+LIB = _lib.lib()
+LIB.tn_debug_orth_bench.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+for m, n, nb in [(8192, 128, 2), (8192, 128, 1), (4096, 128, 2), (1024, 64, 16), (2048, 32, 16)]:
+    out = np.zeros(2)
+    assert LIB.tn_debug_orth_bench(m, n, nb, 20, 0, out.ctypes.data) == 0
+    print(f"orth m={m} n={n} nb={nb} old={os.environ.get('TN_ORTH_OLD', '0')}: {out[0]:.3f} ms", flush=True)
