@@ -42,28 +42,49 @@ struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaStream_t s = nullptr;
+  // Optional device float: an upper bound of max |component| over the buffer's complex
+  // contents, written by the tensor-core GEMM that produced them (lets a consumer GEMM scale
+  // its FP16 operand planes without a max pass). It lives in `tail` spare bytes allocated
+  // after the data (no separate allocation); any in-place write must drop it.
+  float* tail = nullptr;
+  bool amax_valid = false;
   DevBuf() = default;
-  DevBuf(size_t n, cudaStream_t st) { alloc(n, st); }
-  void alloc(size_t n, cudaStream_t st) {
+  DevBuf(size_t n, cudaStream_t st, bool with_tail = false) { alloc(n, st, with_tail); }
+  void alloc(size_t n, cudaStream_t st, bool with_tail = false) {
     release();
     s = st;
     bytes = n;
-    if (n) TN_CUDA(cudaMallocAsync(&p, n, st));
+    if (n) {
+      const size_t pad = with_tail ? 256 : 0;
+      TN_CUDA(cudaMallocAsync(&p, n + pad, st));
+      if (with_tail) tail = reinterpret_cast<float*>(reinterpret_cast<char*>(p) + ((n + 15) / 16) * 16);
+    }
   }
+  float* amax() const { return amax_valid ? tail : nullptr; }
+  float* make_amax() {  // the producing GEMM zeroes it (stream order) before writing
+    if (!tail) return nullptr;
+    amax_valid = true;
+    return tail;
+  }
+  void drop_amax() { amax_valid = false; }
   void release() {
     if (p) cudaFreeAsync(p, s);
     p = nullptr;
+    tail = nullptr;
+    amax_valid = false;
     bytes = 0;
   }
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; o.bytes = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s), tail(o.tail), amax_valid(o.amax_valid) {
+    o.p = nullptr; o.bytes = 0; o.tail = nullptr; o.amax_valid = false;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; bytes = o.bytes; s = o.s;
-      o.p = nullptr; o.bytes = 0;
+      p = o.p; bytes = o.bytes; s = o.s; tail = o.tail; amax_valid = o.amax_valid;
+      o.p = nullptr; o.bytes = 0; o.tail = nullptr; o.amax_valid = false;
     }
     return *this;
   }

@@ -66,6 +66,8 @@ struct TcParams {
   int64_t sc1, sc2;
   int z0;
   int accumulate;
+  const float* amax_uniform;  // non-null: one scale for all rows of A (max over the tensor)
+  float* amax_out;            // non-null: atomicMax of max |component| of the stored C values
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -142,6 +144,23 @@ __device__ __forceinline__ int scale_exp(float mx) {
 __device__ __forceinline__ float inv_scale(float mx) {
   if (!(mx > 0.f)) return 1.f;
   return ldexpf(1.f, scale_exp(mx));
+}
+
+// Many warps update one address: read first and only issue the atomic when it would raise
+// the value (same-address atomics serialise in L2).
+__device__ __forceinline__ void atomic_max_nonneg(float* p, float v) {
+  if (v > 0.f && v > *reinterpret_cast<volatile float*>(p))
+    atomicMax(reinterpret_cast<unsigned int*>(p), __float_as_uint(v));
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ float row_amax(const TcParams& p, int z, int row) {
+  return p.amax_uniform ? *p.amax_uniform : p.amax[(int64_t)z * p.Mp + row];
 }
 
 // Grouped rasterisation: linear tile id -> (m, n), groups of RASTER_GM m-tiles swept with m
@@ -277,8 +296,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
+    float lmax = 0.f;
     if (row < p.M) {
-      const float rs = inv_scale(p.amax[(int64_t)z * p.Mp + row]);
+      const float rs = inv_scale(row_amax(p, z, row));
       const float* bmx = p.bmax + (int64_t)bz * p.Np;
       const int n0 = (nblk * TC_BN + half * 128) >> 1;
       if (p.ksplit > 1) {  // partial sum of this K split -> workspace
@@ -306,9 +326,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               val.y += o.y;
             }
             Crow[n] = val;
+            lmax = fmaxf(lmax, fmaxf(fabsf(val.x), fabsf(val.y)));
           }
         }
       }
+    }
+    if (p.amax_out && p.ksplit == 1) {
+      lmax = warp_max(lmax);
+      if (lane == 0) atomic_max_nonneg(p.amax_out, lmax);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -547,7 +572,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       {
         const int z = tl.z, bz = p.b_batched ? z : 0;
         const int row0 = (tl.mblk0 + (int)rank) * 128 + lg * 32;
-        const float rs = (row < p.M) ? inv_scale(p.amax[(int64_t)z * p.Mp + row]) : 0.f;
+        const float rs = (row < p.M) ? inv_scale(row_amax(p, z, row)) : 0.f;
+        float lmax = 0.f;
         const float* bmx = p.bmax + (int64_t)bz * p.Np;
         const int n0 = (tl.nblk * TC_BN + half * 128) >> 1;
         float2* base;
@@ -586,9 +612,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                 val.y += o.y;
               }
               *dst = val;
+              lmax = fmaxf(lmax, fmaxf(fabsf(val.x), fabsf(val.y)));
             }
           }
           __syncwarp();
+        }
+        if (p.amax_out && p.ksplit == 1) {
+          lmax = warp_max(lmax);
+          if (lane == 0) atomic_max_nonneg(p.amax_out, lmax);
         }
       }
     }
@@ -603,8 +634,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 // Deterministic split-K reduction: C (+)= sum over splits in a fixed order.
 __global__ void splitk_reduce_kernel(const float2* __restrict__ ws, int ksplit, int64_t ws_split, int nz, int M,
                                      int N, float2* C, int64_t cm, int nb2, int64_t sc1, int64_t sc2, int z0,
-                                     int accumulate) {
+                                     int accumulate, float* amax_out) {
   const int64_t per = (int64_t)M * N, tot = per * nz;
+  float lmax = 0.f;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t zz = e / per, r = e - zz * per;
     const int row = (int)(r / N), n = (int)(r - (int64_t)row * N);
@@ -623,6 +655,11 @@ __global__ void splitk_reduce_kernel(const float2* __restrict__ ws, int ksplit, 
       s.y += o.y;
     }
     *cp = s;
+    lmax = fmaxf(lmax, fmaxf(fabsf(s.x), fabsf(s.y)));
+  }
+  if (amax_out) {
+    lmax = warp_max(lmax);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(amax_out, lmax);
   }
 }
 
@@ -650,6 +687,8 @@ struct PrepArgs {
   int z0, R, K, Rrows, Krp;  // Rrows: padded plane rows (A: Mp; B: Nrp)
   int k_fast;
   float* mx;                 // [z][Rp] row maxima (max pass writes, prep reads)
+  const float* mx_uniform;   // non-null: one maximum for every row (no max pass)
+  float* zero_me;            // non-null: set to 0 by block (0,0,0) (the GEMM's output maximum)
   int Rp;                    // row count of mx per z (complex rows)
   __half* hi;
   __half* lo;
@@ -690,6 +729,7 @@ __device__ __forceinline__ const float2* prep_base(const PrepArgs& a, int zz) {
 // Pass 1: max |component| of every row over K (atomicMax on the IEEE bits of a non-negative
 // float is order-independent, hence deterministic).
 __global__ void __launch_bounds__(256) rowmax_kernel(PrepArgs a) {
+  if (a.zero_me && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *a.zero_me = 0.f;
   __shared__ float2 tile[32][33];
   __shared__ int64_t roff[32], koff[PK_K];
   const int r0 = blockIdx.y * 32, k0 = blockIdx.x * PK_K, zz = blockIdx.z;
@@ -744,7 +784,7 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
   if (t >= 224) {
     const int i = t - 224;
-    const float m = (r0 + i < a.R) ? a.mx[(int64_t)zz * a.Rp + r0 + i] : 0.f;
+    const float m = (r0 + i < a.R) ? (a.mx_uniform ? *a.mx_uniform : a.mx[(int64_t)zz * a.Rp + r0 + i]) : 0.f;
     scl[i] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
   }
   prep_offsets(a, roff, koff, r0, k0);
@@ -959,6 +999,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     a.Krp = Krp;
     a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
     a.mx = bmx.as<float>();
+    a.mx_uniform = nullptr;
+    a.zero_me = g.amaxC;
     a.Rp = Np;
     a.hi = bh.as<__half>();
     a.lo = bl.as<__half>();
@@ -986,6 +1028,10 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     kbps = ((kblocks + ksplit - 1) / ksplit + TC_KC - 1) / TC_KC * TC_KC;
     ksplit = (kblocks + kbps - 1) / kbps;
   }
+  // A's scale: one exponent for the whole operand when its producer recorded max |component|
+  // (no row-max pass; error per element <= 2^-24 of that maximum), else per row.
+  static const bool uniform_off = getenv("TN_ROWSCALE") && std::atoi(getenv("TN_ROWSCALE")) != 0;
+  const bool use_uniform = g.amaxA != nullptr && !uniform_off;
   // ---- A planes, chunked over the batch to bound the workspace (<= ~1 GB per plane)
   const int64_t per_z = (int64_t)Mp * Krp;
   const int zc = (int)std::max<int64_t>(
@@ -1013,13 +1059,17 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       a.Krp = Krp;
       a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
       a.mx = amx.as<float>();
+      a.mx_uniform = use_uniform ? g.amaxA : nullptr;
+      a.zero_me = nullptr;
       a.Rp = Mp;
       a.hi = ah.as<__half>();
       a.lo = al.as<__half>();
-      TN_CUDA(cudaMemsetAsync(amx.p, 0, (size_t)nz * Mp * sizeof(float), c.stream));
-      dim3 gmax(ceil_div(g.K, PK_K), ceil_div(g.M, 32), nz);
-      rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
-      TN_LAUNCHED();
+      if (!use_uniform) {
+        TN_CUDA(cudaMemsetAsync(amx.p, 0, (size_t)nz * Mp * sizeof(float), c.stream));
+        dim3 gmax(ceil_div(g.K, PK_K), ceil_div(g.M, 32), nz);
+        rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
+        TN_LAUNCHED();
+      }
       dim3 grid(ceil_div(Krp / 2, PK_K), Mp / 32, nz);
       prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
       TN_LAUNCHED();
@@ -1046,6 +1096,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.sc2 = g.sc2;
     p.z0 = z0;
     p.accumulate = g.accumulate ? 1 : 0;
+    p.amax_uniform = use_uniform ? g.amaxA : nullptr;
+    p.amax_out = g.amaxC;
     if (slog && z0 == 0) cudaEventRecord(srec.b, c.stream);
     {
       ProfScope ps(P_TC_KERNEL, c.stream);
@@ -1097,7 +1149,7 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       int64_t tot = (int64_t)nz * g.M * g.N;
       unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16);
       splitk_reduce_kernel<<<blocks, 256, 0, c.stream>>>(p.ws, ksplit, ws_split, nz, g.M, g.N, g.C, g.cm, g.nb2,
-                                                         g.sc1, g.sc2, z0, p.accumulate);
+                                                         g.sc1, g.sc2, z0, p.accumulate, g.amaxC);
       TN_LAUNCHED();
     }
   }

@@ -209,6 +209,7 @@ void hash_init(Ctx& c, Tensor& o, int nb, uint64_t seed, int tag, int b1, int k)
 }
 
 void normalize(Ctx& c, Tensor& t, int nb, double* logn, bool acc) {
+  invalidate_amax(t);
   ProfScope ps(P_MISC, c.stream);
   int n = t.bstride ? nb : 1;
   int64_t size = t.size();
@@ -273,6 +274,7 @@ Tensor ones(Ctx& c, const std::vector<int>& shape, int nb) {
 }
 
 void copy_rows(Ctx& c, const Tensor& src, Tensor& dst, int64_t x0, int nb) {
+  invalidate_amax(dst);
   int64_t rowsz = dst.size() / dst.shape[0];
   int n = src.bstride ? nb : 1;
   int64_t size = src.size();
@@ -281,6 +283,7 @@ void copy_rows(Ctx& c, const Tensor& src, Tensor& dst, int64_t x0, int nb) {
 }
 
 void add_into(Ctx& c, Tensor& dst, const Tensor& src, int nb) {
+  invalidate_amax(dst);
   int n = dst.bstride ? nb : 1;
   int64_t size = dst.size();
   add_kernel<<<grid_for(size * n), 256, 0, c.stream>>>(dst.p, dst.bstride, src.p, src.bstride, size, n);

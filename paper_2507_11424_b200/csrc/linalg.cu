@@ -7,6 +7,7 @@
 #include "linalg.h"
 
 namespace tn {
+__device__ long long g_chol_clk[8];  // debugging: phase clocks of the last chol_smem_kernel (block 0)
 namespace {
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -524,6 +525,7 @@ __device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; } 
 // pass is needed: rank deficiency, or a pivot ratio l_11 / l_nn > 1e3 (an estimate of the
 // condition number; below it the single pass, with its Gram exact in FP64 for FP32 data,
 // is orthogonal to ~kappa^2 1e-16 < FP32 rounding).
+
 template <bool PIVOT>
 __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __restrict__ part, int splits, int n,
                                                                double tol, double2* __restrict__ Wall,
@@ -543,6 +545,7 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
   __shared__ int s_piv, s_rank;
   __shared__ double s_dp, s_d0;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const long long clk0 = clock64();
   const int64_t nn = (int64_t)n * n;
   const double2* P0 = part + (int64_t)b * splits * nn;
   // load the lower triangle (sum of the split partials, fixed order)
@@ -572,6 +575,7 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
     }
   }
   __syncthreads();
+  const long long clk1 = clock64();
   const double d0 = s_d0;
   const double floor_d = 1e-300 + 1e-30 * d0;
   for (int k = 0; k < n; ++k) {
@@ -656,6 +660,7 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
     __syncthreads();
   }
   __syncthreads();
+  const long long clk2 = clock64();
   const int rank = s_rank;
   if (PIVOT && t == 0) {
     rank_all[b] = rank;
@@ -712,7 +717,14 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
     }
     __syncwarp();
   }
+  __syncthreads();
+  if (b == 0 && t == 0) {
+    g_chol_clk[0] = clk1 - clk0;
+    g_chol_clk[1] = clk2 - clk1;
+    g_chol_clk[2] = clock64() - clk2;
+  }
 }
+
 
 }  // namespace
 
@@ -932,3 +944,8 @@ void orthonormalize(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, in
 }
 
 }  // namespace tn
+
+// debugging: clocks of the last chol_smem_kernel's block 0: load, factorisation, inverse
+extern "C" int tn_debug_chol_clocks(long long* out) {
+  return cudaMemcpyFromSymbol(out, tn::g_chol_clk, 3 * sizeof(long long)) == cudaSuccess ? 0 : -1;
+}

@@ -23,7 +23,7 @@ Tensor new_tensor_n(Ctx& c, const std::vector<int>& shape, int nb) {
   int64_t sz = prod(shape);
   t.bstride = nb > 1 ? sz : (nb == 1 ? sz : 0);
   size_t bytes = (size_t)std::max<int64_t>(1, sz * std::max(nb, 1)) * sizeof(float2);
-  t.mem = std::make_shared<DevBuf>(bytes, c.stream);
+  t.mem = std::make_shared<DevBuf>(bytes, c.stream, true);
   t.p = t.mem->as<float2>();
   return t;
 }
@@ -35,6 +35,7 @@ Tensor new_tensor(Ctx& c, const std::vector<int>& shape, bool per_sample) {
 }
 
 void zero(Ctx& c, Tensor& t, int nb) {
+  invalidate_amax(t);
   int64_t n = t.bstride ? t.bstride * nb : t.size();
   TN_CUDA(cudaMemsetAsync(t.p, 0, (size_t)n * sizeof(float2), c.stream));
 }
@@ -346,18 +347,18 @@ __global__ void __launch_bounds__(256) cgemm_simt(GemmDesc g) {
 }
 }  // namespace
 
-void gemm(Ctx& c, const GemmDesc& g) {
-  if (g.M <= 0 || g.N <= 0 || g.nb1 <= 0 || g.nb2 <= 0) return;
+bool gemm(Ctx& c, const GemmDesc& g) {
+  if (g.M <= 0 || g.N <= 0 || g.nb1 <= 0 || g.nb2 <= 0) return false;
   g_cmacs += (double)g.M * g.N * std::max(g.K, 0) * g.nb1 * g.nb2;
   if (g.K <= 0) {
     if (!g.accumulate) {
       // C = 0 (empty contraction): handled by the planner allocating zeroed outputs
     }
-    return;
+    return false;
   }
   {
     ProfScope ps(P_GEMM_TC, c.stream);
-    if (c.gemm_mode != 1 && gemm_tc(c, g)) return;
+    if (c.gemm_mode != 1 && gemm_tc(c, g)) return true;
   }
   ProfScope ps(P_GEMM_SIMT, c.stream);
   int64_t nbz = (int64_t)g.nb1 * g.nb2;
@@ -373,7 +374,7 @@ void gemm(Ctx& c, const GemmDesc& g) {
       gemm(c, h);
     }
     g_cmacs -= (double)g.M * g.N * g.K * g.nb1 * g.nb2;
-    return;
+    return false;
   }
   dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, BM), (unsigned)nbz);
   if (grid.y > 65535) {
@@ -386,10 +387,11 @@ void gemm(Ctx& c, const GemmDesc& g) {
       gemm(c, h);
       g_cmacs -= (double)h.M * h.N * h.K * h.nb1 * h.nb2;
     }
-    return;
+    return false;
   }
   cgemm_simt<<<grid, 256, 0, c.stream>>>(g);
   TN_LAUNCHED();
+  return false;
 }
 
 // ----------------------------------------------------------------------------- planner
@@ -644,7 +646,11 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
     g.M = (int)(Msz * g.nb1);
     g.nb1 = 1;
   }
-  gemm(c, g);
+  // operand / output magnitude bounds (tensor-core path): A's bound spares its row-max pass
+  if (Xu == &X) g.amaxA = tensor_amax(X);
+  if (C.mem && !g.accumulate) g.amaxC = C.mem->make_amax();
+  const bool tc = gemm(c, g);
+  if (!tc && C.mem) C.mem->drop_amax();
   if (direct) return C;
   std::string gl = gout.empty() ? std::string("?") : gout;
   // permute to requested order (including unit dims)
@@ -656,6 +662,10 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
   for (char ch : src) Ct.shape.push_back(dim.count(ch) ? dim[ch] : 1);
   if (gl == "?") { Ct.shape = oshape; return Ct; }
   Tensor R = permute(c, Ct, src.c_str(), dst.c_str(), false);
+  if (C.mem && C.mem->amax() && R.mem && R.mem->tail) {  // same values, new layout
+    TN_CUDA(cudaMemcpyAsync(R.mem->tail, C.mem->tail, sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+    R.mem->make_amax();
+  }
   return R;
 }
 

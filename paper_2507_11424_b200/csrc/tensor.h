@@ -25,6 +25,13 @@ struct Tensor {
   int rank() const { return (int)shape.size(); }
 };
 
+// max |component| bound of a tensor's memory (nullptr if unknown) and its invalidation, to be
+// called by every in-place write (see DevBuf::amax).
+inline const float* tensor_amax(const Tensor& t) { return t.mem ? t.mem->amax() : nullptr; }
+inline void invalidate_amax(const Tensor& t) {
+  if (t.mem) t.mem->drop_amax();
+}
+
 struct Ctx {
   cudaStream_t stream = nullptr;
   int gemm_mode = 0;  // 0 auto, 1 SIMT only, 2 tcgen05 whenever legal
@@ -72,8 +79,11 @@ struct GemmDesc {
   bool accumulate = false;
   int64_t work_per_sample = 0;  // complex MACs of one sample (kernel choice must not depend on batch)
   int m_per_sample = 0;         // M before the sample batch was folded into it
+  const float* amaxA = nullptr;  // max |component| bound of all of A (skips A's row-max pass)
+  float* amaxC = nullptr;        // if set: receives max |component| of C (tensor-core path only)
 };
-void gemm(Ctx& c, const GemmDesc& g);
+// Returns true when the tensor-core path ran (and filled g.amaxC if set).
+bool gemm(Ctx& c, const GemmDesc& g);
 // Whether gemm() will route a GEMM of this per-sample shape to the tensor cores.
 bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per_sample);
 

@@ -12,3 +12,8 @@ for m, n, nb in [(8192, 128, 2), (8192, 128, 1), (4096, 128, 2), (1024, 64, 16),
     out = np.zeros(2)
     assert LIB.tn_debug_orth_bench(m, n, nb, 20, 0, out.ctypes.data) == 0
     print(f"orth m={m} n={n} nb={nb} old={os.environ.get('TN_ORTH_OLD', '0')}: {out[0]:.3f} ms", flush=True)
+LIB.tn_debug_chol_clocks.argtypes = [C.c_void_p]
+clk = np.zeros(3, dtype=np.int64)
+LIB.tn_debug_orth_bench(8192, 128, 1, 1, 0, np.zeros(2).ctypes.data)
+LIB.tn_debug_chol_clocks(clk.ctypes.data)
+print("chol clocks (load, factor, inverse) of the last call:", clk.tolist())

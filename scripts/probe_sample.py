@@ -34,9 +34,10 @@ stream = torch.cuda.current_stream(dev)
 N = lat.n
 for nb in batches:
     g.set_option("max_batch", nb)
-    u = torch.from_numpy(np.random.default_rng(5).random((4, nb, N))).to(dev)
-    bits = torch.empty((4, nb, N), dtype=torch.uint8, device=dev)
-    lq = torch.empty((4, nb), dtype=torch.float64, device=dev)
+    T = int(os.environ.get("PROBE_STEPS", "2"))
+    u = torch.from_numpy(np.random.default_rng(5).random((2 + T, nb, N))).to(dev)
+    bits = torch.empty((2 + T, nb, N), dtype=torch.uint8, device=dev)
+    lq = torch.empty((2 + T, nb), dtype=torch.float64, device=dev)
 
     def step(s):
         g.sample_dev(lat.rows, R, nb, u[s].data_ptr(), bits[s].data_ptr(), lq[s].data_ptr(), 0, 0,
@@ -52,16 +53,16 @@ for nb in batches:
     LIB.tn_debug_counters(cnt.ctypes.data, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    step(2)
-    step(3)
+    for s_ in range(2, 2 + T):
+        step(s_)
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / 2
+    ms = e0.elapsed_time(e1) / T
     LIB.tn_debug_profile(prof.ctypes.data, None, 7, 1)
     LIB.tn_debug_set_profile(0)
     LIB.tn_debug_counters(cnt.ctypes.data, 1)
-    ph = {k: round(float(v) / 2, 1) for k, v in zip(bench.PHASES, prof)}
-    print(f"batch {nb}: {ms:.1f} ms/step, {1000 * nb / ms:.3f} samples/s, cMAC/sample {cnt[0] / (2 * nb):.3e}; "
+    ph = {k: round(float(v) / T, 1) for k, v in zip(bench.PHASES, prof)}
+    print(f"batch {nb}: {ms:.1f} ms/step, {1000 * nb / ms:.3f} samples/s, cMAC/sample {cnt[0] / (T * nb):.3e}; "
           f"phases ms/step {ph}", flush=True)
 if os.environ.get("TN_GEMM_LOG"):
     LIB.tn_debug_gemm_log()
