@@ -833,6 +833,58 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
   }
 }
 
+// A planes when K is the contiguous axis of the operand (innermost K view stride 1, even
+// extent): no shared-memory transpose -- each thread streams 2 consecutive complex k of one
+// row (one 16-byte load) into one half2x2 (8-byte) store per plane, 8 rows per CTA.
+constexpr int PKF_ROWS = 8;
+constexpr int PKF_PAIRS = 256;  // k pairs per CTA (= threads)
+__global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
+  __shared__ int64_t roff[PKF_ROWS];
+  __shared__ float scl[PKF_ROWS];
+  const int r0 = blockIdx.y * PKF_ROWS, zz = blockIdx.z;
+  const int t = threadIdx.x;
+  if (t < PKF_ROWS) {
+    const int r = r0 + t;
+    roff[t] = (r < a.R) ? view_off(a.vr, r) : -1;
+    const float m = (r < a.R) ? (a.mx_uniform ? *a.mx_uniform : a.mx[(int64_t)zz * a.Rp + r]) : 0.f;
+    scl[t] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
+  }
+  const int kpair = blockIdx.x * PKF_PAIRS + t;  // complex k = 2 kpair, 2 kpair + 1
+  const int k = 2 * kpair;
+  const bool in_plane = 2 * k < a.Krp;           // plane columns 2k .. 2k+3
+  const bool in_k = k < a.K;                      // K even on this path: k + 1 < K too
+  const int64_t ko = in_k ? view_off(a.vk, k) : 0;
+  __syncthreads();
+  if (!in_plane) return;
+  const float2* base = prep_base(a, zz);
+  const int64_t plane = (int64_t)a.Rrows * a.Krp;
+  uint2* hi = reinterpret_cast<uint2*>(a.hi + zz * plane);
+  uint2* lo = reinterpret_cast<uint2*>(a.lo + zz * plane);
+  const int kq = a.Krp >> 2;  // uint2 (4 halves) per plane row
+#pragma unroll
+  for (int j = 0; j < PKF_ROWS; ++j) {
+    const int r = r0 + j;
+    if (r >= a.Rrows) break;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (in_k && roff[j] >= 0) v = *reinterpret_cast<const float4*>(base + roff[j] + ko);
+    if (a.conj) {
+      v.y = -v.y;
+      v.w = -v.w;
+    }
+    const float sc = scl[j];
+    __half2 h0, l0, h1, l1;
+    split16x2(v.x * sc, v.y * sc, h0, l0);
+    split16x2(v.z * sc, v.w * sc, h1, l1);
+    uint2 hv, lv;
+    hv.x = *reinterpret_cast<uint32_t*>(&h0);
+    hv.y = *reinterpret_cast<uint32_t*>(&h1);
+    lv.x = *reinterpret_cast<uint32_t*>(&l0);
+    lv.y = *reinterpret_cast<uint32_t*>(&l1);
+    hi[(int64_t)r * kq + kpair] = hv;
+    lo[(int64_t)r * kq + kpair] = lv;
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1070,8 +1122,21 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
         rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
         TN_LAUNCHED();
       }
-      dim3 grid(ceil_div(Krp / 2, PK_K), Mp / 32, nz);
-      prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
+      // K-contiguous operands (innermost K stride 1, even length, 16-byte aligned base and
+      // row/batch offsets) take the transpose-free kernel
+      const View4& vk = a.vk;
+      bool kfast = vk.rank > 0 && vk.str[vk.rank - 1] == 1 && vk.dims[vk.rank - 1] % 2 == 0 && g.K % 2 == 0 &&
+                   (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 && a.s1 % 2 == 0 && a.s2 % 2 == 0;
+      for (int d = 0; d < vk.rank - 1 && kfast; ++d) kfast = vk.str[d] % 2 == 0;
+      for (int d = 0; d < a.vr.rank && kfast; ++d) kfast = a.vr.str[d] % 2 == 0 || a.vr.dims[d] == 1;
+      static const bool kfast_off = getenv("TN_PREP_KFAST") && std::atoi(getenv("TN_PREP_KFAST")) == 0;
+      if (kfast && !kfast_off) {
+        dim3 grid(ceil_div(Krp / 4, PKF_PAIRS), ceil_div(Mp, PKF_ROWS), nz);
+        prep_kfast_kernel<<<grid, 256, 0, c.stream>>>(a);
+      } else {
+        dim3 grid(ceil_div(Krp / 2, PK_K), Mp / 32, nz);
+        prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
+      }
       TN_LAUNCHED();
     }
     CUtensorMap mah = make_map(ah.as<__half>(), Krp, Mp, nz, TC_BM);

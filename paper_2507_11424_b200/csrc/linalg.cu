@@ -578,6 +578,10 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
   const long long clk1 = clock64();
   const double d0 = s_d0;
   const double floor_d = 1e-300 + 1e-30 * d0;
+  // Right-looking Cholesky, two block barriers per step: warp 0 picks the pivot, forms the
+  // column of L and updates the remaining diagonal (dg); then every warp applies the rank-1
+  // update to the strictly lower part of the remaining block.
+  __shared__ int s_brk;
   for (int k = 0; k < n; ++k) {
     if (warp == 0) {
       int p = k;
@@ -603,60 +607,61 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
       } else {
         dp = dg[k];
       }
+      bool brk = false;
+      if (PIVOT) {
+        brk = !(dp > tol * d0) || d0 <= 0;
+      } else if (!(dp > floor_d)) {
+        if (lane == 0) atomicOr(bad, 1);
+        dp = floor_d;
+      }
+      if (!brk) {
+        const double lkk = sqrt(dp);
+        const double inv = 1.0 / lkk;
+        for (int i = lane; i < n; i += 32) {
+          if (i == p) {
+            S[pk(p, p)] = make_double2(lkk, 0);
+            lv[i] = make_double2(0, 0);
+          } else if (alive[i]) {
+            double2 g = i > p ? S[pk(i, p)] : S[pk(p, i)];
+            if (i < p) g.y = -g.y;  // G(i, p) = conj(G(p, i))
+            const double2 l = make_double2(g.x * inv, g.y * inv);
+            lv[i] = l;
+            if (i > p) S[pk(i, p)] = l;
+            else S[pk(p, i)] = make_double2(l.x, -l.y);
+            dg[i] -= l.x * l.x + l.y * l.y;
+          } else {
+            lv[i] = make_double2(0, 0);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          alive[p] = 0;
+          perm[k] = p;
+        }
+      }
       if (lane == 0) {
         s_piv = p;
-        s_dp = dp;
+        s_brk = brk ? 1 : 0;
+        if (brk) s_rank = k;
       }
     }
     __syncthreads();
+    if (s_brk) break;
     const int p = s_piv;
-    double dp = s_dp;
-    if (PIVOT) {
-      if (!(dp > tol * d0) || d0 <= 0) {
-        if (t == 0) s_rank = k;
-        break;
-      }
-    } else if (!(dp > floor_d)) {
-      if (t == 0) atomicOr(bad, 1);
-      dp = floor_d;
-    }
-    const double lkk = sqrt(dp);
-    const double inv = 1.0 / lkk;
-    // column of L for the remaining indices: l_i = G(i, p) / lkk (stored back in place)
-    for (int i = t; i < n; i += CH_THREADS) {
-      if (i == p) {
-        S[pk(p, p)] = make_double2(lkk, 0);
-        lv[i] = make_double2(0, 0);
-      } else if (alive[i]) {
-        double2 g = i > p ? S[pk(i, p)] : S[pk(p, i)];
-        if (i < p) g.y = -g.y;  // G(i, p) = conj(G(p, i))
-        double2 l = make_double2(g.x * inv, g.y * inv);
-        lv[i] = l;
-        if (i > p) S[pk(i, p)] = l;
-        else S[pk(p, i)] = make_double2(l.x, -l.y);
-      } else {
-        lv[i] = make_double2(0, 0);
-      }
-    }
-    __syncthreads();
-    if (t == 0) {
-      alive[p] = 0;
-      perm[k] = p;
-    }
-    // Schur complement on the remaining indices (lower triangle): G(i,j) -= l_i conj(l_j)
+    // Schur complement, strictly lower part of the remaining block: G(i,j) -= l_i conj(l_j)
     for (int i = warp; i < n; i += CH_THREADS / 32) {
-      if (i == p || !alive[i]) continue;
+      if (!alive[i]) continue;
       const double2 li = lv[i];
-      for (int j = lane; j <= i; j += 32) {
-        if (j == p || !alive[j]) continue;
+      for (int j = lane; j < i; j += 32) {
+        if (!alive[j]) continue;
         const double2 lj = lv[j];
         double2 g = S[pk(i, j)];
         g.x -= li.x * lj.x + li.y * lj.y;
         g.y -= li.y * lj.x - li.x * lj.y;
         S[pk(i, j)] = g;
-        if (i == j) dg[i] = g.x;
       }
     }
+    (void)p;
     __syncthreads();
   }
   __syncthreads();
@@ -678,44 +683,57 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
     if (rank < n) return;  // completion path
   }
   // L(i, k) in pivot order = G(perm[i], perm[k]) (i > k); L(k, k) = G(perm[k], perm[k]).
-  // Linv column j by forward substitution (one warp per column), W[perm[k]][j] = conj(Linv[j][k]).
+  // Column j of Linv by forward substitution, one warp per column, right-looking: lane l owns
+  // rows l, l+32, l+64, l+96 (running sums in registers); once y_k is known (owner lane,
+  // multiplied by the stored 1/L(k,k)) it is broadcast and every lane updates its later rows.
+  // W = P L^-H: W[perm[j]][k] = conj(Linv(k, j)).
+  double* dinv = dg;  // the remaining-diagonal array is free now: 1 / L(k, k) in pivot order
+  for (int k = t; k < n; k += CH_THREADS) dinv[k] = 1.0 / S[pk(perm[k], perm[k])].x;
+  __syncthreads();
   double2* W = Wall + (int64_t)b * nn;
-  double2* y = Y + warp * CH_MAXN;
+  int prow[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) prow[q] = (lane + 32 * q < n) ? perm[lane + 32 * q] : 0;
   for (int jj = warp; jj < n; jj += CH_THREADS / 32) {
     // balance: warp w takes columns w, 2*32-1-w, ... (long and short columns)
     const int blk = jj / (CH_THREADS / 32), w = jj % (CH_THREADS / 32);
     const int sz = min(CH_THREADS / 32, n - blk * (CH_THREADS / 32));
     const int j = (blk & 1) ? blk * (CH_THREADS / 32) + (sz - 1 - w) : jj;
     const int pj = perm[j];
-    if (lane == 0) y[j] = make_double2(1.0 / S[pk(pj, pj)].x, 0);
-    __syncwarp();
-    for (int i = j + 1; i < n; ++i) {
-      const int pi = perm[i];
-      double sx = 0, sy = 0;
-      for (int k = j + lane; k < i; k += 32) {
+    double2* Wrow = W + (int64_t)pj * n;
+    double2 acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = lane + 32 * q;
+      acc[q] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+      if (i < j && i < n) Wrow[i] = make_double2(0, 0);
+    }
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+      if (kb * 32 >= n) break;
+      for (int kl = 0; kl < 32; ++kl) {
+        const int k = kb * 32 + kl;
+        if (k >= n) break;
+        if (k < j) continue;
+        const double ax = __shfl_sync(0xffffffffu, acc[kb].x, kl);
+        const double ay = __shfl_sync(0xffffffffu, acc[kb].y, kl);
+        const double dk = dinv[k];
+        const double2 yk = make_double2(ax * dk, ay * dk);
+        if (lane == kl) Wrow[k] = make_double2(yk.x, -yk.y);
         const int pkk = perm[k];
-        double2 l = pi > pkk ? S[pk(pi, pkk)] : S[pk(pkk, pi)];
-        if (pi < pkk) l.y = -l.y;
-        const double2 yk = y[k];
-        sx += l.x * yk.x - l.y * yk.y;
-        sy += l.x * yk.y + l.y * yk.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = lane + 32 * q;
+          if (q >= kb && i > k && i < n) {
+            const int pi = prow[q];
+            double2 l = pi > pkk ? S[pk(pi, pkk)] : S[pk(pkk, pi)];
+            if (pi < pkk) l.y = -l.y;
+            acc[q].x -= l.x * yk.x - l.y * yk.y;
+            acc[q].y -= l.x * yk.y + l.y * yk.x;
+          }
+        }
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        sy += __shfl_xor_sync(0xffffffffu, sy, o);
-      }
-      if (lane == 0) {
-        const double lii = S[pk(pi, pi)].x;
-        y[i] = make_double2(-sx / lii, -sy / lii);
-      }
-      __syncwarp();
     }
-    // y = Linv(:, j); W = P L^-H: W[perm[j]][k] = conj(Linv(k, j))
-    for (int k = lane; k < n; k += 32) {
-      double2 v = k >= j ? make_double2(y[k].x, -y[k].y) : make_double2(0, 0);
-      W[(int64_t)pj * n + k] = v;
-    }
-    __syncwarp();
   }
   __syncthreads();
   if (b == 0 && t == 0) {
