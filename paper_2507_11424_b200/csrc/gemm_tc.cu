@@ -357,7 +357,8 @@ constexpr int B2_TILE = 128 * TC_BK * 2;                 // 16 KB per CTA (half 
 constexpr int STAGE2_BYTES = 2 * A2_TILE + 2 * B2_TILE;  // 64 KB
 constexpr int EPI_Q = 8;                                 // complex columns per staged store step
 constexpr int EPI_STAGE_BYTES = 8 * 32 * (EPI_Q + 1) * 8;  // per-warp 32 x (8+1) float2 (8 warps)
-constexpr int SMEM2_BYTES = T2_STAGES * STAGE2_BYTES + EPI_STAGE_BYTES + 1024 + 256;
+constexpr int EPI_COLSC_BYTES = 8 * 64 * 4;                 // per-warp column scales of a tile
+constexpr int SMEM2_BYTES = T2_STAGES * STAGE2_BYTES + EPI_STAGE_BYTES + EPI_COLSC_BYTES + 1024 + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -442,6 +443,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float2* epi_stage = reinterpret_cast<float2*>(smem + T2_STAGES * STAGE2_BYTES + 256);
+  float* epi_colsc = reinterpret_cast<float*>(smem + T2_STAGES * STAGE2_BYTES + 256 + EPI_STAGE_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -589,13 +591,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           acc_out = p.accumulate != 0;
         }
         float2* stg = epi_stage + (warp - 2) * 32 * (EPI_Q + 1);
+        // the tile's 64 column scales, once per warp (all lanes share the columns)
+        float* csc = epi_colsc + (warp - 2) * 64;
+        {
+          const int na = n0 + lane, nb = n0 + lane + 32;
+          csc[lane] = (na < p.N) ? inv_scale(bmx[na]) : 0.f;
+          csc[lane + 32] = (nb < p.N) ? inv_scale(bmx[nb]) : 0.f;
+        }
+        __syncwarp();
         const int sub = lane >> 3, col = lane & 7;
 #pragma unroll
         for (int q0 = 0; q0 < 64; q0 += EPI_Q) {
 #pragma unroll
           for (int q = 0; q < EPI_Q; ++q) {
-            const int n = n0 + q0 + q;
-            const float sc = (n < p.N) ? rs * inv_scale(bmx[n]) : 0.f;
+            const float sc = rs * csc[q0 + q];
             stg[lane * (EPI_Q + 1) + q] = make_float2(acc[2 * (q0 + q)] * sc, acc[2 * (q0 + q) + 1] * sc);
           }
           __syncwarp();

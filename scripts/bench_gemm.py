@@ -11,7 +11,7 @@ LIB = _lib.lib()
 LIB.tn_debug_gemm_bench.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
 LIB.tn_debug_last_error.restype = C.c_char_p
 shapes = [(32768, 4096, 4096, 2), (16384, 2048, 1024, 4), (8192, 128, 4096, 8), (4096, 4096, 4096, 1),
-          (128, 4096, 4096, 4), (300, 2048, 2048, 2)]
+          (128, 4096, 4096, 4), (300, 2048, 2048, 2), (8192, 16384, 128, 2), (16384, 4096, 128, 2)]
 modes = [int(x) for x in os.environ.get("MODES", "2,1").split(",")]
 # warm the clocks up (~1-2 s of GEMMs) before timing
 out = np.zeros(4)
