@@ -191,3 +191,21 @@ def test_certify_matches_oracle_metrics():
     assert stt["n_used"] == len(u) and stt["n_excluded"] == 0
     # unbiasedness: the estimate is within a few standard errors of <psi|psi>
     assert abs(math.exp(stt["log_norm_estimate"] - lz) - 1) < 5 * stt["norm_rel_stderr"] + 1e-6
+
+
+def test_config2_vs_oracle():
+    """BASELINE config 2 (6x6 square, domain-wall Heisenberg quench, 5 layers, chi = 8,
+    chi_env = 32) at finite chi_env: per-sample conditionals, ln q and bits against the oracle
+    (R16) on the same seeded state and uniforms; U(1) pass rate reported."""
+    lat, st = G.config_state("cfg2")
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, 32)
+    u = S.uniforms(256, lat.n, 1002)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 32, u)
+    rb, rl, rc = oracle_samples(P, M, 32, u, 8)
+    rep = compare_samples(order_of(lat.rows), u[:8], bits[:8], logq[:8], cond[:8], rb, rl, rc)
+    assert rep["compared"] > 0
+    assert np.isfinite(logq).all() and (flags & 4 == 0).all()
+    # truncation keeps the magnetisation sector for most samples (PAPER.md:174: > 96 % at R = 3)
+    ok = (bits.sum(axis=1) == sum(L.domain_wall_bits(lat))).mean()
+    assert ok > 0.9, ok
