@@ -12,6 +12,9 @@ a Tensor Network State"), with the readings of SURVEY 8(c) listed in DESIGN.md:
                     as the product of the conditionals              [O5]
 * amplitude()       <x|psi> by projected-row fits          [O6]
 * log_norm()        <psi|psi> = <M_{2->1}, T_1> (R12)
+* sample_literal()  the paper's own within-row order:
+                    sample row b against the uncompressed m_{b-1} . psi_b, its conjugate
+                    and M_{b+1->b} (a five-layer ladder), then fit m_b = Fit_R(m_{b-1} . X_b)
 
 Notation: rows b = 0..N_b-1 (0-based here; the init hash uses the 1-based b of the
 paper), columns j = 0..W_b-1 in row order, A_v[s, u, d, l, r] (SURVEY 8 notation).
@@ -27,7 +30,7 @@ from .rows import site_tensors
 
 MASK64 = (1 << 64) - 1
 DEFAULT_SEED = 0x2507114240
-TAG_N, TAG_M, TAG_AMP = 1, 2, 3
+TAG_N, TAG_M, TAG_AMP, TAG_LIT = 1, 2, 3, 4
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -482,3 +485,74 @@ def amplitude(P: Prepared, bits, R: int, seed: int = DEFAULT_SEED, nh: int = 2):
                 return -math.inf, 0.0
             return logs + math.log(abs(s)), math.atan2(s.imag, s.real)
     raise RuntimeError("last row has down edges")
+
+
+def sample_literal(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2, forced=None):
+    """NEXT-3: the paper's literal order. Row b is sampled qubit by qubit
+    from the one-site reduced density matrices of the five-layer ladder
+    m_{b-1->b} . psi_b . conj(psi_b) . conj(m_{b-1->b}) . M_{b+1->b} (sampled qubits projected
+    on both layers, later ones traced), then m_{b->b+1} = Fit_R(m_{b-1->b} . X_b) with
+    X_b = x_b . psi_b and the down legs open (tag 4). Same draw rule, clamp and ln q as
+    sample() (R9, R10). Exact when R_x, R_n are exact.
+    Right env R_j[a, l, L, A, e]: m bond, ket / bra row bond, conj(m) bond, M bond."""
+    n = P.n
+    bits = np.zeros(n, dtype=np.uint8)
+    cond = np.zeros(n, dtype=np.float64)
+    logq = 0.0
+    flags = 0
+    m_prev = None
+    for b, row in enumerate(P.rows):
+        W = len(row)
+        ms = _tops_for_row(P, row, m_prev, "up", "single")     # [a, u, b] (identity: u = 1)
+        Ms = _tops_for_row(P, row, M[b], "down", "double")     # [e, d, D, f]
+        As = [P.A[v] for v in row]                              # [s, u, d, l, r]
+
+        def right_site(R_next, j, s=None):
+            # R_next[b, r, R, B, f] -> R_j[(s,) a, l, L, A, e]
+            T1 = pair(R_next, "brRBf", ms[j], "aub", "rRBfau")
+            T2 = pair(T1, "rRBfau", As[j], "sudlr", "RBfasdl")
+            T3 = pair(T2, "RBfasdl", Ms[j], "edDf", "RBasleD")
+            T4 = pair(T3, "RBasleD", As[j].conj(), "sUDLR", "sBaleUL")
+            T5 = pair(T4, "sBaleUL", ms[j].conj(), "AUB", "salLAe")
+            return T5 if s is None else T5[s]
+
+        Rs = [None] * W
+        Rr = np.ones((1, 1, 1, 1, 1), dtype=np.complex128)
+        for j in range(W - 1, -1, -1):
+            Rs[j] = right_site(Rr, j)                           # [s, a, l, L, A, e]
+            tot = Rs[j][0] + Rs[j][1]
+            scale = np.abs(tot).max()
+            Rr = tot / scale if scale > 0 else tot  # [a, l, L, A, e] = [b, r, R, B, f] of column j-1
+        Lx = np.ones((1, 1, 1, 1, 1), dtype=np.complex128)      # [a, l, L, A, e]
+        for j, v in enumerate(row):
+            w = [float(np.real(np.sum(Lx * Rs[j][s]))) for s in range(2)]
+            if w[0] < 0 or w[1] < 0:
+                flags |= 1
+            w = [max(x, 0.0) for x in w]
+            tot = w[0] + w[1]
+            if tot > 0:
+                p0 = w[0] / tot
+            else:
+                flags |= 2
+                p0 = 0.5
+            x = (0 if u_row[v] < p0 else 1) if forced is None else int(forced[v])
+            px = p0 if x == 0 else 1.0 - p0
+            bits[v] = x
+            cond[v] = px
+            logq += math.log(px) if px > 0 else -math.inf
+            # L_{j+1}[b, r, R, B, f] = L_j . m_j . A_j[x] . M_j . conj(A_j[x]) . conj(m_j)
+            G1 = pair(Lx, "alLAe", ms[j], "aub", "lLAeub")
+            G2 = pair(G1, "lLAeub", As[j][x], "udlr", "LAebdr")
+            G3 = pair(G2, "LAebdr", Ms[j], "edDf", "LAbrDf")
+            G4 = pair(G3, "LAbrDf", As[j][x].conj(), "UDLR", "AbrfUR")
+            Lx = pair(G4, "AbrfUR", ms[j].conj(), "AUB", "brRBf")
+            scale = np.abs(Lx).max()
+            if scale > 0:
+                Lx = Lx / scale
+        if b + 1 < len(P.rows):
+            mats = [P.A[v][int(bits[v])] for v in row]                       # [u, d, l, r]
+            out = [P.has(v, "down") for v in row]
+            res, _ = fit(Strip("single", ms, mats, out), R, TAG_LIT, b + 1, seed, nh)
+            m_prev = res if isinstance(res, list) else None
+    return bits, logq, cond, flags
+

@@ -418,3 +418,49 @@ def test_kld_worked_example():
     assert abs(metrics.kld(np.log(q), np.log(p)) - want) < 1e-15
     # identity observable -> 1 exactly
     assert abs(metrics.importance_expectation(np.log(q), np.log(p), [1, 1]) - 1) < 1e-15
+
+
+# ---------------------------------------------------------------- NEXT-3: paper-literal order
+def _all_q_literal(P, M, R, n):
+    qs = {}
+    for x in itertools.product([0, 1], repeat=n):
+        bits, logq, cond, _ = B.sample_literal(P, M, R, np.zeros(n), forced=np.array(x))
+        qs[x] = math.exp(logq)
+    return qs
+
+
+def test_literal_order_exact_regime_is_statevector():
+    """the paper's own order (sample against the uncompressed m.psi_b, then
+    fit) is exact when R is exact: q(x) = |<x|psi>|^2 / <psi|psi> for all 512 x of config 1
+    and the drawn conditionals equal the statevector conditionals."""
+    lat, st = G.config_state("cfg1")
+    psi = SV.statevector(st)
+    p = np.abs(psi) ** 2 / np.vdot(psi, psi).real
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, 16)
+    qs = _all_q_literal(P, M, 16, lat.n)
+    for x, q in qs.items():
+        assert abs(q - p[int("".join(map(str, x)), 2)]) < 1e-12
+    u = S.uniforms(8, lat.n, 1001)
+    for k in range(8):
+        bits, logq, cond, fl = B.sample_literal(P, M, 16, u[k])
+        ref = SV.conditionals(psi, lat.n, order_of(lat.rows), bits)
+        assert np.allclose([cond[v] for v in order_of(lat.rows)], ref, rtol=1e-10)
+
+
+def test_literal_order_truncated_is_normalised_and_differs():
+    """At finite R the literal order's q is a distribution too (sum_x q = 1, so E_q[p/q] =
+    <psi|psi>), and it differs from compress-then-sample (R3): the two
+    orders coincide only in the exact regime."""
+    lat = L.square(3, 3)
+    st = S.vidal_like(lat, 3, seed=9, xi=4.0)
+    psi = SV.statevector(st)
+    p = np.abs(psi) ** 2
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, 2)
+    ql = _all_q_literal(P, M, 2, lat.n)
+    assert abs(sum(ql.values()) - 1) < 1e-12
+    est = sum(q * p[int("".join(map(str, x)), 2)] / q for x, q in ql.items() if q > 0)
+    assert abs(est - p.sum()) < 1e-12 * p.sum()
+    qc = _all_q(P, M, 2, lat.n)
+    assert max(abs(ql[x] - qc[x]) for x in ql) > 1e-6
