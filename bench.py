@@ -41,6 +41,8 @@ WORKLOADS = {
     "willow105_chi8_env32": ("willow105", 8, 32, 256),
     "eagle127_chi16_env64": ("eagle127", 16, 64, 64),
     "square6x6_chi8_env32": ("square6x6", 8, 32, 512),
+    # the paper's literal order is meant for chi_env <= chi (R <= 20 with chi >= 20)
+    "willow105_chi8_env8": ("willow105", 8, 8, 256),
 }
 PHASES = ["gemm_tc_incl_prep", "gemm_simt", "permute", "orth", "tail", "misc", "tc_kernel"]
 DEFAULT_WORKLOAD = "willow105_chi32_env128"
@@ -230,6 +232,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0, help="samples per GPU per step (0 = workload default)")
+    ap.add_argument("--order", type=int, default=0, choices=[0, 1],
+                    help="0: compress-then-sample (R3, default); 1: the paper's literal order (NEXT-3, R <= chi)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
@@ -245,6 +249,7 @@ def main():
     lat = L.by_name(lat_name)
     config = {"workload": a.workload, "lattice": lat_name, "n_qubits": lat.n, "chi": chi, "chi_env": R,
               "samples_per_gpu_per_step": batch, "fit_half_sweeps": 2, "row_order": "lattice rows",
+              "within_row_order": "paper-literal (NEXT-3)" if a.order else "compress-then-sample (R3)",
               "state": "synthetic Vidal-gauge-like TNS (dense, singular-value-weighted bonds, every bond at chi)",
               "l2": "L2 flushed between timed steps (256 MB write); per-step working set >> 126 MB"}
 
@@ -289,6 +294,8 @@ def main():
     if world > 1:
         st = broadcast_state(st, lat, chi, rank, dist, torch, dev)
     g = TNState(st)
+    if a.order:
+        g.set_option("order", a.order)
     t_load = time.time() - t0
     t0 = time.time()
     pre_prof = np.zeros(7)

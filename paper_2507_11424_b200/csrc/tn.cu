@@ -59,6 +59,7 @@ struct tn_state {
   cudaStream_t stream = nullptr;
   Ctx ctx;
   int nh = 2;
+  int order = 0;  // 0: compress-then-sample (R3); 1: the paper's literal order (NEXT-3)
   uint64_t seed = 0x2507114240ull;
   int64_t max_batch = 0;
   std::map<std::string, std::unique_ptr<Layout>> layouts;
@@ -398,6 +399,95 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
   }
 }
 
+// Identity "top" for a column without an incoming MPS site: [bond, 1, bond] (single layer)
+// or [bond, 1, 1, bond] (double layer), shared by all samples.
+Tensor identity_top(Ctx& c, int bond, bool dbl) {
+  std::vector<float2> h((size_t)bond * bond, make_float2(0.f, 0.f));
+  for (int i = 0; i < bond; ++i) h[(size_t)i * bond + i] = make_float2(1.f, 0.f);
+  Tensor t = new_tensor(c, dbl ? std::vector<int>{bond, 1, 1, bond} : std::vector<int>{bond, 1, bond}, false);
+  TN_CUDA(cudaMemcpyAsync(t.p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice, c.stream));
+  TN_CUDA(cudaStreamSynchronize(c.stream));  // h is a host temporary
+  return t;
+}
+
+// NEXT-3 for one batch (oracle sample_literal): the paper's literal order
+// (PAPER.md:289-290). Row b is sampled from the five-layer ladder m_{b-1}.psi_b.conj(psi_b).
+// conj(m_{b-1}).M_{b+1->b} (right env [b, r, R, B, f]: m bond, ket / bra row bond, conj(m)
+// bond, M bond), then m_b = Fit_R(m_{b-1}.X_b), X_b = x_b.psi_b with the down legs open
+// (tag 4). Same tail (draw, clamp, ln q) as O5. Feasible where R <= chi (the paper's runs):
+// the environment has R_x^2 R_n chi^2 entries.
+void sample_batch_literal(tn_state* st, Layout& L, Envs& E, int R, int nb, const double* u_dev, uint8_t* bits_dev,
+                          double* logq_dev, double* cond_dev, uint32_t* flags_dev) {
+  Ctx& c = st->ctx;
+  c.nb = nb;
+  int N = st->n;
+  TN_CUDA(cudaMemsetAsync(logq_dev, 0, sizeof(double) * nb, c.stream));
+  TN_CUDA(cudaMemsetAsync(flags_dev, 0, sizeof(uint32_t) * nb, c.stream));
+  DevBuf xbuf(sizeof(int) * nb, c.stream);
+  std::vector<Tensor> m_prev;
+  bool have_prev = false;
+  for (int b = 0; b < (int)L.rows.size(); ++b) {
+    const auto& row = L.rows[b];
+    const int W = (int)row.size();
+    DStrip ms, Ms;
+    place_tops(L, b, have_prev ? &m_prev : nullptr, 0, ms);
+    place_tops(L, b, E.M[b].empty() ? nullptr : &E.M[b], 1, Ms);
+    std::vector<Tensor> mj(W), Mj(W);
+    for (int j = 0; j < W; ++j) {
+      mj[j] = ms.tops[j].p ? ms.tops[j] : identity_top(c, ms.topbond[j], false);
+      Mj[j] = Ms.tops[j].p ? Ms.tops[j] : identity_top(c, Ms.topbond[j], true);
+    }
+    // right pass: Rs[j][s, a, l, L, A, e]
+    std::vector<Tensor> Rs(W);
+    Tensor Rr = ones(c, {1, 1, 1, 1, 1}, nb);
+    for (int j = W - 1; j >= 0; --j) {
+      const Tensor& A = L.A[row[j]];
+      Tensor T1 = contract(c, Rr, "brRBf", false, mj[j], "aub", false, "rRBfau");
+      Tensor T2 = contract(c, T1, "rRBfau", false, A, "sudlr", false, "RBfasdl");
+      Tensor T3 = contract(c, T2, "RBfasdl", false, Mj[j], "edDf", false, "RBasleD");
+      Tensor T4 = contract(c, T3, "RBasleD", false, A, "sUDLR", true, "sBaleUL");
+      Rs[j] = contract(c, T4, "sBaleUL", false, mj[j], "AUB", true, "salLAe");
+      if (j > 0) {
+        Rr = sum2(c, Rs[j]);
+        normalize(c, Rr, nb, nullptr, false);
+      }
+    }
+    // left pass + draw
+    Tensor Lx = ones(c, {1, 1, 1, 1, 1}, nb);
+    std::vector<Tensor> Ax(W);
+    for (int j = 0; j < W; ++j) {
+      const int v = row[j];
+      TailOut to{xbuf.as<int>(), bits_dev, logq_dev, cond_dev, flags_dev, u_dev, N, v};
+      tail_draw(c, Lx, Rs[j], nb, to);
+      Rs[j] = Tensor{};
+      Ax[j] = gather_bit(c, L.A[v], bits_dev, N, v, nb);  // A_v[x_v] = [u, d, l, r] per sample
+      if (j + 1 < W) {
+        Tensor G1 = contract(c, Lx, "alLAe", false, mj[j], "aub", false, "lLAeub");
+        Tensor G2 = contract(c, G1, "lLAeub", false, Ax[j], "udlr", false, "LAebdr");
+        Tensor G3 = contract(c, G2, "LAebdr", false, Mj[j], "edDf", false, "LAbrDf");
+        Tensor G4 = contract(c, G3, "LAbrDf", false, Ax[j], "UDLR", true, "AbrfUR");
+        Lx = contract(c, G4, "AbrfUR", false, mj[j], "AUB", true, "brRBf");
+        normalize(c, Lx, nb, nullptr, false);
+      }
+    }
+    // m_b = Fit_R(m_{b-1} . X_b), down legs open
+    if (b + 1 < (int)L.rows.size()) {
+      DStrip s;
+      s.dbl = false;
+      s.per_sample = true;
+      s.W = W;
+      place_tops(L, b, have_prev ? &m_prev : nullptr, 0, s);
+      for (int j = 0; j < W; ++j) {
+        s.mats.push_back(Ax[j]);
+        s.out.push_back(has(L, row[j], 1));
+      }
+      FitResult fr = fit(c, s, R, 4, b + 1, st->seed, st->nh, nullptr, false);
+      m_prev = fr.sites;
+      have_prev = !m_prev.empty();
+    }
+  }
+}
+
 // O6 for one batch: ln|<x|psi>| and phase.
 void amplitude_batch(tn_state* st, Layout& L, int R, int nb, const uint8_t* bits_dev, double* logabs,
                      double* phase) {
@@ -522,7 +612,8 @@ void sample_common(tn_state* st, const int32_t* row_ptr, const int32_t* rv, int3
         fd = fb.as<uint32_t>();
         cd = cond ? cb.as<double>() : nullptr;
       }
-      sample_batch(st, L, E, chi_env, nb, ud, bd, ld, cd, fd);
+      if (st->order == 1) sample_batch_literal(st, L, E, chi_env, nb, ud, bd, ld, cd, fd);
+      else sample_batch(st, L, E, chi_env, nb, ud, bd, ld, cd, fd);
       if (!out_on_device) {
         TN_CUDA(cudaMemcpyAsync(bits + done * N, bd, (size_t)nb * N, cudaMemcpyDeviceToHost, c.stream));
         TN_CUDA(cudaMemcpyAsync(logp + done, ld, sizeof(double) * nb, cudaMemcpyDeviceToHost, c.stream));
@@ -621,6 +712,10 @@ int tn_set_option(tn_state* st, const char* name, int64_t value) {
     } else if (k == "gemm") {
       if (value < 0 || value > 2) throw Error(TN_E_ARG, "gemm must be 0, 1 or 2");
       st->ctx.gemm_mode = (int)value;
+    } else if (k == "order") {
+      if (value < 0 || value > 1) throw Error(TN_E_ARG, "order must be 0 (compress-then-sample) or 1 (literal)");
+      st->order = (int)value;
+      return;
     } else if (k == "max_batch") {
       st->max_batch = value;
       return;

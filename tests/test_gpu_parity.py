@@ -209,3 +209,60 @@ def test_config2_vs_oracle():
     # truncation keeps the magnetisation sector for most samples (> 96 % at R = 3)
     ok = (bits.sum(axis=1) == sum(L.domain_wall_bits(lat))).mean()
     assert ok > 0.9, ok
+
+
+def _run_literal(st, rows, R, u):
+    g = TNState(st)
+    g.set_option("order", 1)
+    bits, logq, cond, flags = g.sample(rows, R, u, want_cond=True)
+    return g, bits, logq, cond, flags
+
+
+def test_literal_order_exact_regime_vs_statevector():
+    """NEXT-3: the paper's own order on the GPU, exact regime -> the
+    statevector conditionals and ln q."""
+    lat = L.square(3, 3)
+    st = S.vidal_like(lat, 2, seed=3, xi=2.0)
+    psi = SV.statevector(st)
+    u = S.uniforms(32, lat.n, 5)
+    g, bits, logq, cond, flags = _run_literal(st, lat.rows, 16, u)
+    order = order_of(lat.rows)
+    for k in range(len(u)):
+        ref = SV.conditionals(psi, lat.n, order, bits[k])
+        assert np.allclose([cond[k, v] for v in order], ref, rtol=1e-4, atol=1e-6), k
+        idx = int("".join(map(str, bits[k])), 2)
+        lp = math.log(abs(psi[idx]) ** 2 / np.vdot(psi, psi).real)
+        assert abs(logq[k] - lp) <= 1e-4 * max(1, abs(lp))
+
+
+@pytest.mark.parametrize("R", [4, 2])
+def test_literal_order_truncated_vs_oracle(R):
+    """NEXT-3 at finite chi_env (config 1 state): GPU vs oracle.sample_literal (R16)."""
+    lat, st = G.config_state("cfg1")
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, R)
+    u = S.uniforms(32, lat.n, 1001)
+    g, bits, logq, cond, flags = _run_literal(st, lat.rows, R, u)
+    rb = np.zeros((len(u), lat.n), np.uint8)
+    rl = np.zeros(len(u))
+    rc = np.zeros((len(u), lat.n))
+    for k in range(len(u)):
+        rb[k], rl[k], rc[k], _ = B.sample_literal(P, M, R, u[k])
+    rep = compare_samples(order_of(lat.rows), u, bits, logq, cond, rb, rl, rc)
+    assert rep["compared"] > 0
+
+
+def test_literal_order_willow_topology():
+    """NEXT-3 on the full Willow-105 topology (chi = 2, chi_env = 4) against the oracle."""
+    lat = L.willow105()
+    st = S.vidal_like(lat, 2, seed=21, xi=2.0)
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, 4)
+    u = S.uniforms(4, lat.n, 31)
+    g, bits, logq, cond, flags = _run_literal(st, lat.rows, 4, u)
+    rb = np.zeros((len(u), lat.n), np.uint8)
+    rl = np.zeros(len(u))
+    rc = np.zeros((len(u), lat.n))
+    for k in range(len(u)):
+        rb[k], rl[k], rc[k], _ = B.sample_literal(P, M, 4, u[k])
+    compare_samples(order_of(lat.rows), u, bits, logq, cond, rb, rl, rc)
