@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(256) rowmax_kernel(PrepArgs a) {
   if (a.zero_me && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *a.zero_me = 0.f;
   __shared__ float2 tile[32][33];
   __shared__ int64_t roff[32], koff[PK_K];
-  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * PK_K, zz = blockIdx.z;
+  const int r0 = blockIdx.x * 32, k0 = blockIdx.y * PK_K, zz = blockIdx.z;  // rows on x (2^31 limit)
   prep_offsets(a, roff, koff, r0, k0);
   const float2* base = prep_base(a, zz);
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
   __shared__ float2 tile[32][33];
   __shared__ int64_t roff[32], koff[PK_K];
   __shared__ float scl[32];
-  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * PK_K, zz = blockIdx.z;
+  const int r0 = blockIdx.x * 32, k0 = blockIdx.y * PK_K, zz = blockIdx.z;  // rows on x
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
   if (t >= 224) {
     const int i = t - 224;
@@ -850,7 +850,7 @@ constexpr int PKF_PAIRS = 256;  // k pairs per CTA (= threads)
 __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
   __shared__ int64_t roff[PKF_ROWS];
   __shared__ float scl[PKF_ROWS];
-  const int r0 = blockIdx.y * PKF_ROWS, zz = blockIdx.z;
+  const int r0 = blockIdx.x * PKF_ROWS, zz = blockIdx.z;  // rows on x (2^31 limit)
   const int t = threadIdx.x;
   if (t < PKF_ROWS) {
     const int r = r0 + t;
@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
     const float m = (r < a.R) ? (a.mx_uniform ? *a.mx_uniform : a.mx[(int64_t)zz * a.Rp + r]) : 0.f;
     scl[t] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
   }
-  const int kpair = blockIdx.x * PKF_PAIRS + t;  // complex k = 2 kpair, 2 kpair + 1
+  const int kpair = blockIdx.y * PKF_PAIRS + t;  // complex k = 2 kpair, 2 kpair + 1
   const int k = 2 * kpair;
   const bool in_plane = 2 * k < a.Krp;           // plane columns 2k .. 2k+3
   const bool in_k = k < a.K;                      // K even on this path: k + 1 < K too
@@ -1065,10 +1065,10 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     a.Rp = Np;
     a.hi = bh.as<__half>();
     a.lo = bl.as<__half>();
-    dim3 gmax(ceil_div(g.K, PK_K), ceil_div(g.N, 32), nzb);
+    dim3 gmax(ceil_div(g.N, 32), ceil_div(g.K, PK_K), nzb);
     rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
-    dim3 grid(ceil_div(Krp / 2, PK_K), Nrp / 64, nzb);
+    dim3 grid(Nrp / 64, ceil_div(Krp / 2, PK_K), nzb);
     prep_tiled_kernel<1><<<grid, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
   }
@@ -1127,7 +1127,7 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       a.lo = al.as<__half>();
       if (!use_uniform) {
         TN_CUDA(cudaMemsetAsync(amx.p, 0, (size_t)nz * Mp * sizeof(float), c.stream));
-        dim3 gmax(ceil_div(g.K, PK_K), ceil_div(g.M, 32), nz);
+        dim3 gmax(ceil_div(g.M, 32), ceil_div(g.K, PK_K), nz);
         rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
         TN_LAUNCHED();
       }
@@ -1140,10 +1140,10 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       for (int d = 0; d < a.vr.rank && kfast; ++d) kfast = a.vr.str[d] % 2 == 0 || a.vr.dims[d] == 1;
       static const bool kfast_off = getenv("TN_PREP_KFAST") && std::atoi(getenv("TN_PREP_KFAST")) == 0;
       if (kfast && !kfast_off) {
-        dim3 grid(ceil_div(Krp / 4, PKF_PAIRS), ceil_div(Mp, PKF_ROWS), nz);
+        dim3 grid(ceil_div(Mp, PKF_ROWS), ceil_div(Krp / 4, PKF_PAIRS), nz);
         prep_kfast_kernel<<<grid, 256, 0, c.stream>>>(a);
       } else {
-        dim3 grid(ceil_div(Krp / 2, PK_K), Mp / 32, nz);
+        dim3 grid(Mp / 32, ceil_div(Krp / 2, PK_K), nz);
         prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
       }
       TN_LAUNCHED();
