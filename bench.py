@@ -187,7 +187,41 @@ class LazyRandomM:
         return self.cache[b]
 
 
-def oracle_rate(st, lat, R, row_cmacs, budget_s, seed=7):
+def oracle_row_cmacs(P, M, R):
+    """Complex MACs per row of one oracle sample, counted on the oracle's own pairwise
+    contractions (oracle.bmps.pair) in a shape-only dry run: every pair() returns zeros of
+    the output shape, so the whole sample costs milliseconds. The oracle's arithmetic is
+    untouched (the dry run replaces the function only for the duration of the count)."""
+    from oracle import bmps as B
+    counts = []
+    real_pair = B.pair
+
+    def dry_pair(a, sa, b, sb, out):
+        dims = {}
+        for lab, t in ((sa, a), (sb, b)):
+            for ch, d in zip(lab, t.shape):
+                dims[ch] = d
+        cm = 1.0
+        for d in dims.values():
+            cm *= d
+        counts[-1] += cm
+        return np.zeros([dims[ch] for ch in out], dtype=np.complex128)
+
+    rows_total = len(P.rows)
+    per_row = []
+    B.pair = dry_pair
+    try:
+        with np.errstate(all="ignore"):
+            for r in range(1, rows_total + 1):
+                counts.append(0.0)
+                B.sample(P, M, R, np.zeros(P.n), forced=np.zeros(P.n, dtype=np.uint8), max_rows=r)
+                per_row.append(counts[-1] - sum(per_row))
+    finally:
+        B.pair = real_pair
+    return per_row
+
+
+def oracle_rate(st, lat, R, row_cmacs, budget_s, seed=7, workload=None):
     """Bounded timing of the CPU oracle (oracle/bmps.sample, as it stands) on the same
     workload: rows are sampled in order until the budget is spent; samples/s is scaled by
     the fraction of one sample's algorithmic complex MACs those rows carry."""
@@ -200,6 +234,13 @@ def oracle_rate(st, lat, R, row_cmacs, budget_s, seed=7):
     t0 = time.time()
     P = B.Prepared(st, lat.rows)
     M = LazyRandomM(P, R, np.random.default_rng(seed))
+    if row_cmacs is None:
+        # per-row complex MACs of the oracle's own contractions (scripts/oracle_row_cmacs.py,
+        # a shape-only dry run of oracle.bmps.sample; recomputed here when not tabulated)
+        try:
+            row_cmacs = json.load(open(os.path.join(ROOT, "profiles", "oracle_row_cmacs.json")))[workload]
+        except Exception:
+            row_cmacs = oracle_row_cmacs(P, M, R)
     setup = time.time() - t0
     u = np.random.default_rng(seed).random(lat.n)
     total = float(sum(row_cmacs)) if row_cmacs else 0.0
@@ -219,9 +260,10 @@ def oracle_rate(st, lat, R, row_cmacs, budget_s, seed=7):
     rate = frac / last if last > 0 else float("nan")
     return {"value": rate, "unit": "samples/s", "cores": int(threads), "kind": "oracle",
             "sample": (f"one sample's first {rows_done}/{len(lat.rows)} rows ({100 * frac:.3g}% of its "
-                       f"algorithmic complex MACs) took {last:.1f} s on the host; samples/s scaled by that "
-                       f"fraction; random norm-environment sites of the method's shapes (oracle precompute "
-                       f"at this size takes days); setup {setup:.0f} s not timed")}
+                       f"complex MACs, counted on the oracle's own contractions by a shape-only dry run) took "
+                       f"{last:.1f} s on the host; samples/s scaled by that fraction; random norm-environment "
+                       f"sites of the method's shapes (oracle precompute at this size takes days); setup "
+                       f"{setup:.0f} s not timed")}
 
 
 def main():
@@ -257,11 +299,12 @@ def main():
         if rank != 0:
             return
         st = make_state(lat, chi)
-        # rows' algorithmic cost shares from the cost model of the method (complex MACs per row)
-        shares = row_shares_model(st, lat, R)
+        # rows' cost shares: complex MACs of the oracle's own contractions, counted by a
+        # shape-only dry run of oracle.bmps.sample (oracle_row_cmacs)
+        shares = None
         vals = []
         for i in range(a.warmup + a.steps):
-            cb = oracle_rate(st, lat, R, shares, budget_s=a.cpu_budget / 2)
+            cb = oracle_rate(st, lat, R, shares, budget_s=a.cpu_budget / 2, workload=a.workload)
             if i >= a.warmup:
                 vals.append(cb["value"])
         v = float(np.mean(vals))
@@ -421,7 +464,7 @@ def main():
            "phase_ms": {k: float(v) for k, v in zip(PHASES, prof)}, "precompute_phase_ms": pre_phase}
     if world == 1 and not a.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = oracle_rate(st, lat, R, list(rows), budget_s=a.cpu_budget)
+            out["cpu_baseline"] = oracle_rate(st, lat, R, None, budget_s=a.cpu_budget, workload=a.workload)
         except Exception as e:  # pragma: no cover
             out["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "oracle",
                                    "sample": f"failed: {e}"}
@@ -430,22 +473,6 @@ def main():
         LIB.tn_debug_gemm_log()
     if dist:
         dist.destroy_process_group()
-
-
-def row_shares_model(st, lat, R):
-    """Per-row complex-MAC shares for the reference arm (no GPU): the leading terms of the
-    ladder (3 chi_d^2 D^4-type GEMMs) and the row fit, per vertex, from the R6 bonds."""
-    from oracle import bmps as B
-    P = B.Prepared(st, lat.rows)
-    shares = []
-    for b, row in enumerate(P.rows):
-        tot = 0.0
-        for v in row:
-            _, u, d, l, r = P.A[v].shape
-            D = min(R, 4 * max(u, d, l, r) ** 2)
-            tot += 3.0 * d * d * D ** 4 + 2.0 * D * D * (2 * d) * u * l * r  # ladder + row fit
-        shares.append(tot)
-    return shares
 
 
 if __name__ == "__main__":

@@ -309,9 +309,11 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
   std::vector<int> D = fit_bonds(s, R);
   std::vector<Tensor> o(K);
   for (int k = 0; k < K; ++k) {
-    o[k] = new_tensor_n(c, o_shape(s, cols[k], D[k], D[k + 1]), nb);
-    if (!s.per_sample) o[k].bstride = 0;
-    hash_init(c, o[k], nb, seed, tag, b1, k);
+    // the initial guess does not depend on the sample (R4: the hash key is (seed, tag, b,
+    // k, i)): one shared copy, right-orthonormalised once for the whole batch below
+    o[k] = new_tensor_n(c, o_shape(s, cols[k], D[k], D[k + 1]), 1);
+    o[k].bstride = 0;
+    hash_init(c, o[k], 1, seed, tag, b1, k);
   }
   // right-orthonormalise as a true gauge transformation (absorb the factor to the left)
   for (int k = K - 1; k >= 1; --k) {
