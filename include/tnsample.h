@@ -135,8 +135,12 @@ int tn_certify(tn_state* st, const uint8_t* bits, const double* logq, int64_t n,
 
 /* Options (SURVEY 5 "Config / flags"): "fit_half_sweeps" (nh, default 2, R5), "init_seed"
  * (default 0x2507114240, R4), "gemm" (0 = auto, 1 = force SIMT FP32, 2 = force tcgen05
- * FP16x3), "max_batch" (0 = auto from free device memory). Changing an option invalidates
- * cached environments. Unknown name -> TN_E_ARG. */
+ * FP16x3), "max_batch" (0 = auto from free device memory), "order" (within-row sampling
+ * order: 0 = compress-then-sample, R3, default; 1 = the paper's literal order, PAPER.md:
+ * 289-290 -- sample row b against the uncompressed m_{b-1}.psi_b five-layer ladder, then fit
+ * the projected row; its environments hold chi_env^3 chi^2 entries, meant for chi_env <=
+ * chi). Changing fit_half_sweeps / init_seed / gemm invalidates cached environments.
+ * Unknown name or value -> TN_E_ARG. */
 int tn_set_option(tn_state* st, const char* name, int64_t value);
 
 /* Kernel launches and wall-clock of the last call on this state (instrumentation). */
