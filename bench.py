@@ -221,49 +221,74 @@ def oracle_row_cmacs(P, M, R):
     return per_row
 
 
-def oracle_rate(st, lat, R, row_cmacs, budget_s, seed=7, workload=None):
+class OracleTimer:
     """Bounded timing of the CPU oracle (oracle/bmps.sample, as it stands) on the same
-    workload: rows are sampled in order until the budget is spent; samples/s is scaled by
-    the fraction of one sample's algorithmic complex MACs those rows carry."""
-    from oracle import bmps as B
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
-    except Exception:
-        threads = os.cpu_count()
-    t0 = time.time()
-    P = B.Prepared(st, lat.rows)
-    M = LazyRandomM(P, R, np.random.default_rng(seed))
-    if row_cmacs is None:
-        # per-row complex MACs of the oracle's own contractions (scripts/oracle_row_cmacs.py,
-        # a shape-only dry run of oracle.bmps.sample; recomputed here when not tabulated)
+    workload: one sample's rows are run in order for as many rows as fit the budget (the row
+    count is chosen once by predicting each extra row's time from its complex MACs, so no run
+    exceeds the budget by more than one row's misprediction); samples/s is scaled by the
+    fraction of the sample's complex MACs those rows carry (counted on the oracle's own
+    contractions, scripts/oracle_row_cmacs.py)."""
+
+    def __init__(self, st, lat, R, budget_s, seed=7, workload=None):
+        from oracle import bmps as B
+        self.B = B
         try:
-            row_cmacs = json.load(open(os.path.join(ROOT, "profiles", "oracle_row_cmacs.json")))[workload]
+            from threadpoolctl import threadpool_info
+            self.threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
         except Exception:
-            row_cmacs = oracle_row_cmacs(P, M, R)
-    setup = time.time() - t0
-    u = np.random.default_rng(seed).random(lat.n)
-    total = float(sum(row_cmacs)) if row_cmacs else 0.0
-    elapsed, rows_done = 0.0, 0
-    t0 = time.time()
-    for r in range(1, len(lat.rows) + 1):
-        B.sample(P, M, R, u, max_rows=r)
-        elapsed = time.time() - t0
-        rows_done = r
-        if elapsed >= budget_s:
-            break
-    # the loop re-runs rows 0..r-1 each time; charge the last run only
-    t1 = time.time()
-    B.sample(P, M, R, u, max_rows=rows_done)
-    last = time.time() - t1
-    frac = (sum(row_cmacs[:rows_done]) / total) if total > 0 else 1.0
-    rate = frac / last if last > 0 else float("nan")
-    return {"value": rate, "unit": "samples/s", "cores": int(threads), "kind": "oracle",
-            "sample": (f"one sample's first {rows_done}/{len(lat.rows)} rows ({100 * frac:.3g}% of its "
-                       f"complex MACs, counted on the oracle's own contractions by a shape-only dry run) took "
-                       f"{last:.1f} s on the host; samples/s scaled by that fraction; random norm-environment "
-                       f"sites of the method's shapes (oracle precompute at this size takes days); setup "
-                       f"{setup:.0f} s not timed")}
+            self.threads = os.cpu_count()
+        t0 = time.time()
+        self.P = B.Prepared(st, lat.rows)
+        self.M = LazyRandomM(self.P, R, np.random.default_rng(seed))
+        try:
+            rc = json.load(open(os.path.join(ROOT, "profiles", "oracle_row_cmacs.json")))[workload]
+        except Exception:
+            rc = oracle_row_cmacs(self.P, self.M, R)
+        self.cum = np.cumsum(np.asarray(rc, dtype=np.float64))
+        self.setup = time.time() - t0
+        self.R = R
+        self.nrows = len(lat.rows)
+        self.u = np.random.default_rng(seed).random(lat.n)
+        # host complex-GEMM rate (one 1024^3 zgemm) as the prior for rows not yet timed
+        a = np.ones((1024, 1024), dtype=np.complex128)
+        t0 = time.time()
+        _ = a @ a
+        zrate = 1024.0 ** 3 / max(time.time() - t0, 1e-6)
+        # choose the row count: at least enough rows to carry 0.01 % of the sample's work (the
+        # first rows are overhead-dominated), then extend while one more row is predicted to fit
+        r = 1
+        while r < self.nrows and self.cum[r - 1] < 1e-4 * self.cum[-1]:
+            r += 1
+        t_r = self.run(r)
+        while r < self.nrows:
+            measured = self.cum[r - 1] / max(t_r, 1e-3) if self.cum[r - 1] > 1e9 else 0.0
+            rate = max(measured, 0.25 * zrate)  # host complex MACs/s
+            pred = t_r + (self.cum[r] - self.cum[r - 1]) / rate
+            if pred > budget_s:
+                break
+            r += 1
+            t_r = self.run(r)
+        self.rows = r
+
+    def run(self, rows):
+        t0 = time.time()
+        self.B.sample(self.P, self.M, self.R, self.u, max_rows=rows)
+        return time.time() - t0
+
+    def measure(self):
+        last = self.run(self.rows)
+        frac = self.cum[self.rows - 1] / self.cum[-1]
+        rate = frac / last if last > 0 else float("nan")
+        return {"value": rate, "unit": "samples/s", "cores": int(self.threads), "kind": "oracle",
+                "sample": (f"one sample's first {self.rows}/{self.nrows} rows ({100 * frac:.3g}% of its complex "
+                           f"MACs, counted on the oracle's own contractions by a shape-only dry run) took "
+                           f"{last:.1f} s on the host; samples/s scaled by that fraction; random norm-environment "
+                           f"sites of the method's shapes (oracle precompute at this size takes days); setup "
+                           f"{self.setup:.0f} s not timed")}
+
+
+def oracle_rate(st, lat, R, budget_s, seed=7, workload=None):
+    return OracleTimer(st, lat, R, budget_s, seed, workload).measure()
 
 
 def main():
@@ -301,10 +326,10 @@ def main():
         st = make_state(lat, chi)
         # rows' cost shares: complex MACs of the oracle's own contractions, counted by a
         # shape-only dry run of oracle.bmps.sample (oracle_row_cmacs)
-        shares = None
+        timer = OracleTimer(st, lat, R, budget_s=a.cpu_budget, workload=a.workload)
         vals = []
         for i in range(a.warmup + a.steps):
-            cb = oracle_rate(st, lat, R, shares, budget_s=a.cpu_budget / 2, workload=a.workload)
+            cb = timer.measure()
             if i >= a.warmup:
                 vals.append(cb["value"])
         v = float(np.mean(vals))
@@ -464,7 +489,7 @@ def main():
            "phase_ms": {k: float(v) for k, v in zip(PHASES, prof)}, "precompute_phase_ms": pre_phase}
     if world == 1 and not a.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = oracle_rate(st, lat, R, None, budget_s=a.cpu_budget, workload=a.workload)
+            out["cpu_baseline"] = oracle_rate(st, lat, R, budget_s=a.cpu_budget, workload=a.workload)
         except Exception as e:  # pragma: no cover
             out["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "oracle",
                                    "sample": f"failed: {e}"}
