@@ -251,9 +251,11 @@ class OracleTimer:
         self.u = np.random.default_rng(seed).random(lat.n)
         # host complex-GEMM rate (one 1024^3 zgemm) as the prior for rows not yet timed
         a = np.ones((1024, 1024), dtype=np.complex128)
+        _ = a @ a
         t0 = time.time()
         _ = a @ a
         zrate = 1024.0 ** 3 / max(time.time() - t0, 1e-6)
+        self.zrate = zrate
         # choose the row count: at least enough rows to carry 0.01 % of the sample's work (the
         # first rows are overhead-dominated), then extend while one more row is predicted to fit
         r = 1
@@ -278,12 +280,20 @@ class OracleTimer:
     def measure(self):
         last = self.run(self.rows)
         frac = self.cum[self.rows - 1] / self.cum[-1]
-        rate = frac / last if last > 0 else float("nan")
+        # extrapolation to the whole sample, taking the faster (CPU-favourable) of: the timed
+        # rows' rate scaled by their work fraction, and the timed rows plus the remaining
+        # complex MACs at the host's full zgemm rate (an upper bound on the oracle's speed)
+        t_scaled = last / frac
+        t_bound = last + (self.cum[-1] - self.cum[self.rows - 1]) / self.zrate
+        t_full = min(t_scaled, t_bound)
+        rate = 1.0 / t_full if t_full > 0 else float("nan")
         return {"value": rate, "unit": "samples/s", "cores": int(self.threads), "kind": "oracle",
                 "sample": (f"one sample's first {self.rows}/{self.nrows} rows ({100 * frac:.3g}% of its complex "
                            f"MACs, counted on the oracle's own contractions by a shape-only dry run) took "
-                           f"{last:.1f} s on the host; samples/s scaled by that fraction; random norm-environment "
-                           f"sites of the method's shapes (oracle precompute at this size takes days); setup "
+                           f"{last:.1f} s on the host; whole sample extrapolated as the faster of the work-fraction "
+                           f"scaling ({t_scaled:.0f} s) and the remaining work at the host's measured zgemm rate "
+                           f"{self.zrate / 1e9:.0f} G complex MAC/s ({t_bound:.0f} s); random norm-environment sites "
+                           f"of the method's shapes (oracle precompute at this size takes days); setup "
                            f"{self.setup:.0f} s not timed")}
 
 
@@ -326,7 +336,9 @@ def main():
         st = make_state(lat, chi)
         # rows' cost shares: complex MACs of the oracle's own contractions, counted by a
         # shape-only dry run of oracle.bmps.sample (oracle_row_cmacs)
-        timer = OracleTimer(st, lat, R, budget_s=a.cpu_budget, workload=a.workload)
+        # each step a bounded sample; the whole run stays within ~4 minutes after setup
+        timer = OracleTimer(st, lat, R, budget_s=min(a.cpu_budget, 240.0 / (a.warmup + a.steps)),
+                            workload=a.workload)
         vals = []
         for i in range(a.warmup + a.steps):
             cb = timer.measure()
