@@ -266,3 +266,31 @@ def test_literal_order_willow_topology():
     for k in range(len(u)):
         rb[k], rl[k], rc[k], _ = B.sample_literal(P, M, 4, u[k])
     compare_samples(order_of(lat.rows), u, bits, logq, cond, rb, rl, rc)
+
+
+@pytest.mark.parametrize("shape", ["one_row", "one_column", "single_vertex"])
+@pytest.mark.parametrize("order", [0, 1])
+def test_degenerate_partitions_vs_statevector(shape, order):
+    """Degenerate line partitions (SURVEY 8(c) edge cases): a chain as one row (no norm
+    environments, no boundary MPS), a chain as one vertex per row (width-1 rows), a single
+    qubit -- exact regime, both within-row orders, against the statevector."""
+    from tninputs.lattices import Lattice
+    n = 1 if shape == "single_vertex" else 6
+    lat = L.chain(n)
+    if shape == "one_row":
+        lat = Lattice("chain_row", n, lat.edges, lat.coords, [list(range(n))], lat.colours)
+    st = S.vidal_like(lat, 2, seed=4, xi=2.0)
+    psi = SV.statevector(st)
+    u = S.uniforms(16, lat.n, 8)
+    g = TNState(st)
+    if order:
+        g.set_option("order", 1)
+    bits, logq, cond, flags = g.sample(lat.rows, 8, u, want_cond=True)
+    order_v = order_of(lat.rows)
+    for k in range(len(u)):
+        ref = SV.conditionals(psi, lat.n, order_v, bits[k])
+        assert np.allclose([cond[k, v] for v in order_v], ref, rtol=1e-4, atol=1e-6), (k, shape)
+    la, ph = g.amplitude(bits[:4], 8)
+    for k in range(4):
+        idx = int("".join(map(str, bits[k])), 2)
+        assert abs(la[k] - math.log(abs(psi[idx]))) < 1e-4
