@@ -412,7 +412,9 @@ def main():
     cnt0 = np.zeros(4)
     LIB.tn_debug_counters(cnt0.ctypes.data, 1)
     prof = np.zeros(7)
-    LIB.tn_debug_set_profile(1)
+    # inside the timed region only the tensor-core GEMM kernels are bracketed by CUDA events
+    # (for the roofline); the per-phase breakdown comes from one extra, untimed step below
+    LIB.tn_debug_set_profile(1 << 6)  # P_TC_KERNEL
     LIB.tn_debug_profile(prof.ctypes.data, None, 7, 1)
     clocks = Clocks(local)
     clocks.start()
@@ -462,6 +464,15 @@ def main():
            "h2d_bytes_per_step": int(batch * N * 8), "d2h_bytes_per_step": int(batch * N * 1 + batch * 8 * 2),
            "steps": e2e_steps}
 
+    # per-phase device time of one extra (untimed) step, every phase bracketed by CUDA events
+    phase = np.zeros(7)
+    LIB.tn_debug_set_profile(1)
+    LIB.tn_debug_profile(phase.ctypes.data, None, 7, 1)
+    step(0)
+    torch.cuda.synchronize()
+    LIB.tn_debug_profile(phase.ctypes.data, None, 7, 1)
+    LIB.tn_debug_set_profile(0)
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -498,7 +509,8 @@ def main():
            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "c64", "data": "synthetic", "config": dict(config, precompute_s=t_pre),
            "roofline": roofline, "e2e": e2e, "gpu_launches": int(cnt[3] - cnt0[3]), "clocks": clk,
-           "phase_ms": {k: float(v) for k, v in zip(PHASES, prof)}, "precompute_phase_ms": pre_phase}
+           "phase_ms_per_step": {k: round(float(v), 1) for k, v in zip(PHASES, phase)},
+           "precompute_phase_ms": pre_phase}
     if world == 1 and not a.no_cpu_baseline:
         try:
             out["cpu_baseline"] = oracle_rate(st, lat, R, budget_s=a.cpu_budget, workload=a.workload)

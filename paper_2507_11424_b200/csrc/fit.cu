@@ -52,7 +52,22 @@ struct Ops {
   }
 
   // ---------------- single layer
+  // mid1(L, j) is needed twice in a left-to-right sweep step (the derivative at k, then the
+  // new left environment from the orthonormalised site): the last result is kept, keyed by
+  // L's memory (held alive, so the address cannot be recycled meanwhile) and the column.
+  Tensor mid1_X;
+  std::shared_ptr<DevBuf> mid1_Lmem;
+  const float2* mid1_Lp = nullptr;
+  int mid1_j = -1;
   Tensor mid1(const Tensor& L, int j) {
+    if (mid1_Lmem && L.mem == mid1_Lmem && L.p == mid1_Lp && j == mid1_j) return mid1_X;
+    mid1_X = mid1_compute(L, j);
+    mid1_Lmem = L.mem;
+    mid1_Lp = L.p;
+    mid1_j = j;
+    return mid1_X;
+  }
+  Tensor mid1_compute(const Tensor& L, int j) {
     const Tensor& B = s.mats[j];
     if (s.tops[j].p) {
       Tensor X1 = contract(c, L, "xmy", false, s.tops[j], "mun", false, "xyun");
@@ -86,8 +101,11 @@ struct Ops {
 
   Tensor absorb_left(const Tensor& L, int j, const Tensor* o) {
     if (!s.dbl) {
+      if (!o) {  // the result becomes an environment that is rescaled in place: not cached
+        Tensor X = mid1_compute(L, j);
+        return view(X, {X.shape[0], X.shape[1], X.shape[3]});
+      }
       Tensor X = mid1(L, j);
-      if (!o) return view(X, {X.shape[0], X.shape[1], X.shape[3]});
       return contract(c, X, "xnpr", false, *o, "xpz", true, "znr");
     }
     int nx = L.shape[0];

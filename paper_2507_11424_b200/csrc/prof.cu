@@ -43,9 +43,12 @@ void Prof::flush() {
 
 }  // namespace tn
 
+// on: 0 = off, 1 = every category, > 1 = bit mask of the categories to record (e.g. only
+// P_TC_KERNEL inside a timed region, keeping the event overhead off the other phases).
 extern "C" int tn_debug_set_profile(int on) {
   tn::g_prof.flush();
   tn::g_prof.on = on != 0;
+  tn::g_prof.mask = on > 1 ? (unsigned)on : ~0u;
   return 0;
 }
 

@@ -12,6 +12,7 @@ enum ProfCat { P_GEMM_TC = 0, P_GEMM_SIMT, P_PERMUTE, P_ORTH, P_TAIL, P_MISC, P_
 
 struct Prof {
   bool on = false;
+  unsigned mask = ~0u;  // categories recorded while on (bit c = ProfCat c)
   struct Rec {
     int cat;
     cudaEvent_t a, b;
@@ -30,7 +31,7 @@ struct ProfScope {
   cudaStream_t s;
   cudaEvent_t a = nullptr;
   ProfScope(int c, cudaStream_t st) : cat(c), s(st) {
-    if (g_prof.on) {
+    if (g_prof.on && ((g_prof.mask >> c) & 1u)) {
       a = g_prof.get();
       cudaEventRecord(a, s);
     }
@@ -40,7 +41,7 @@ struct ProfScope {
       cudaEvent_t b = g_prof.get();
       cudaEventRecord(b, s);
       g_prof.pending.push_back({cat, a, b});
-      if (g_prof.pending.size() > 4096) g_prof.flush();
+      if (g_prof.pending.size() > 65536) g_prof.flush();  // rare: a flush synchronises
     }
   }
 };
