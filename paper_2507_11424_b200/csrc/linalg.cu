@@ -8,6 +8,7 @@
 
 namespace tn {
 __device__ long long g_chol_clk[8];  // debugging: phase clocks of the last chol_smem_kernel (block 0)
+__device__ int g_chol_dbg = 0;       // debugging (timing experiments only): bit 0 skips the Schur update
 namespace {
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -649,7 +650,7 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
     if (s_brk) break;
     const int p = s_piv;
     // Schur complement, strictly lower part of the remaining block: G(i,j) -= l_i conj(l_j)
-    for (int i = warp; i < n; i += CH_THREADS / 32) {
+    for (int i = warp; i < n && !(g_chol_dbg & 1); i += CH_THREADS / 32) {
       if (!alive[i]) continue;
       const double2 li = lv[i];
       for (int j = lane; j < i; j += 32) {
@@ -966,4 +967,8 @@ void orthonormalize(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, in
 // debugging: clocks of the last chol_smem_kernel's block 0: load, factorisation, inverse
 extern "C" int tn_debug_chol_clocks(long long* out) {
   return cudaMemcpyFromSymbol(out, tn::g_chol_clk, 3 * sizeof(long long)) == cudaSuccess ? 0 : -1;
+}
+
+extern "C" int tn_debug_chol_flags(int f) {
+  return cudaMemcpyToSymbol(tn::g_chol_dbg, &f, sizeof(int)) == cudaSuccess ? 0 : -1;
 }

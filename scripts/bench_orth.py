@@ -17,3 +17,9 @@ clk = np.zeros(3, dtype=np.int64)
 LIB.tn_debug_orth_bench(8192, 128, 1, 1, 0, np.zeros(2).ctypes.data)
 LIB.tn_debug_chol_clocks(clk.ctypes.data)
 print("chol clocks (load, factor, inverse) of the last call:", clk.tolist())
+LIB.tn_debug_chol_flags.argtypes = [C.c_int]
+LIB.tn_debug_chol_flags(1)
+LIB.tn_debug_orth_bench(8192, 128, 1, 1, 0, np.zeros(2).ctypes.data)
+LIB.tn_debug_chol_clocks(clk.ctypes.data)
+print("chol clocks without the Schur update:", clk.tolist())
+LIB.tn_debug_chol_flags(0)
