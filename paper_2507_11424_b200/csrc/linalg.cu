@@ -579,90 +579,138 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
   const long long clk1 = clock64();
   const double d0 = s_d0;
   const double floor_d = 1e-300 + 1e-30 * d0;
-  // Right-looking Cholesky, two block barriers per step: warp 0 picks the pivot, forms the
-  // column of L and updates the remaining diagonal (dg); then every warp applies the rank-1
-  // update to the strictly lower part of the remaining block.
-  __shared__ int s_brk;
-  for (int k = 0; k < n; ++k) {
-    if (warp == 0) {
-      int p = k;
-      double dp;
-      if (PIVOT) {
-        double bv = -1;
-        int bi = n;
-        for (int i = lane; i < n; i += 32)
-          if (alive[i] && dg[i] > bv) {
-            bv = dg[i];
-            bi = i;
+  // Right-looking Cholesky with one-step lookahead and one block barrier per step. Warp 0
+  // owns the "column" phase A: for pivot p_k it forms l = G_k(:, p_k) / sqrt(G_k(p_k, p_k)),
+  // stores it (in place and in lvb[k & 1]), updates the remaining diagonal, and picks the next
+  // pivot p_{k+1} from it. Warps 1.. apply the rank-1 update of step k (phase B) to the
+  // strictly lower remaining block except row/column p_{k+1}, while warp 0 already runs phase
+  // A of step k+1 -- it corrects column p_{k+1} by step k's rank-1 term itself.
+  double2* lvb = Y;  // [2][CH_MAXN] column buffers (the per-warp scratch is free here)
+  __shared__ int s_brk, s_next;
+  auto phase_a = [&](int k, int p, const double2* lprev, double2* lcur) {
+    // warp 0 only: column of pivot p (G_k(:,p) = stored column minus the previous step's term)
+    double dp = dg[p];
+    bool brk = false;
+    if (PIVOT) {
+      brk = !(dp > tol * d0) || d0 <= 0;
+    } else if (!(dp > floor_d)) {
+      if (lane == 0) atomicOr(bad, 1);
+      dp = floor_d;
+    }
+    int nxt = n;
+    if (!brk) {
+      const double inv = rsqrt(dp);
+      const double lkk = dp * inv;
+      double2 lpp = make_double2(0, 0);
+      if (lprev) lpp = lprev[p];
+      for (int i = lane; i < n; i += 32) {
+        if (i == p) {
+          S[pk(p, p)] = make_double2(lkk, 0);
+          lcur[i] = make_double2(0, 0);
+        } else if (alive[i]) {
+          double2 g = i > p ? S[pk(i, p)] : S[pk(p, i)];
+          if (i < p) g.y = -g.y;  // G(i, p) = conj(G(p, i))
+          if (lprev) {            // lookahead: step k-1's rank-1 term on column p
+            const double2 li = lprev[i];
+            g.x -= li.x * lpp.x + li.y * lpp.y;
+            g.y -= li.y * lpp.x - li.x * lpp.y;
           }
-        for (int o = 16; o > 0; o >>= 1) {
-          double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
-          }
-        }
-        p = bi;
-        dp = bv;
-      } else {
-        dp = dg[k];
-      }
-      bool brk = false;
-      if (PIVOT) {
-        brk = !(dp > tol * d0) || d0 <= 0;
-      } else if (!(dp > floor_d)) {
-        if (lane == 0) atomicOr(bad, 1);
-        dp = floor_d;
-      }
-      if (!brk) {
-        const double lkk = sqrt(dp);
-        const double inv = 1.0 / lkk;
-        for (int i = lane; i < n; i += 32) {
-          if (i == p) {
-            S[pk(p, p)] = make_double2(lkk, 0);
-            lv[i] = make_double2(0, 0);
-          } else if (alive[i]) {
-            double2 g = i > p ? S[pk(i, p)] : S[pk(p, i)];
-            if (i < p) g.y = -g.y;  // G(i, p) = conj(G(p, i))
-            const double2 l = make_double2(g.x * inv, g.y * inv);
-            lv[i] = l;
-            if (i > p) S[pk(i, p)] = l;
-            else S[pk(p, i)] = make_double2(l.x, -l.y);
-            dg[i] -= l.x * l.x + l.y * l.y;
-          } else {
-            lv[i] = make_double2(0, 0);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          alive[p] = 0;
-          perm[k] = p;
+          const double2 l = make_double2(g.x * inv, g.y * inv);
+          lcur[i] = l;
+          if (i > p) S[pk(i, p)] = l;
+          else S[pk(p, i)] = make_double2(l.x, -l.y);
+          dg[i] -= l.x * l.x + l.y * l.y;
+        } else {
+          lcur[i] = make_double2(0, 0);
         }
       }
+      __syncwarp();
       if (lane == 0) {
-        s_piv = p;
-        s_brk = brk ? 1 : 0;
-        if (brk) s_rank = k;
+        alive[p] = 0;
+        perm[k] = p;
+      }
+      __syncwarp();
+      // next pivot from the updated diagonal
+      if (k + 1 < n) {
+        if (PIVOT) {
+          double bv = -1;
+          int bi = n;
+          for (int i = lane; i < n; i += 32)
+            if (alive[i] && dg[i] > bv) {
+              bv = dg[i];
+              bi = i;
+            }
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+              bv = ov;
+              bi = oi;
+            }
+          }
+          nxt = bi < n ? bi : n;
+          if (bi >= n) nxt = n;  // nothing alive: the rank check of the next step stops
+        } else {
+          nxt = k + 1;
+        }
       }
     }
-    __syncthreads();
+    if (lane == 0) {
+      s_brk = brk ? 1 : 0;
+      if (brk) s_rank = k;
+      s_next = nxt;
+    }
+  };
+  // first pivot and phase A of step 0
+  if (warp == 0) {
+    int p0 = 0;
+    if (PIVOT) {
+      double bv = -1;
+      int bi = n;
+      for (int i = lane; i < n; i += 32)
+        if (dg[i] > bv) {
+          bv = dg[i];
+          bi = i;
+        }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      p0 = bi < n ? bi : 0;
+    }
+    phase_a(0, p0, nullptr, lvb);
+  }
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
     if (s_brk) break;
-    const int p = s_piv;
-    // Schur complement, strictly lower part of the remaining block: G(i,j) -= l_i conj(l_j)
-    for (int i = warp; i < n && !(g_chol_dbg & 1); i += CH_THREADS / 32) {
-      if (!alive[i]) continue;
-      const double2 li = lv[i];
-      for (int j = lane; j < i; j += 32) {
-        if (!alive[j]) continue;
-        const double2 lj = lv[j];
-        double2 g = S[pk(i, j)];
-        g.x -= li.x * lj.x + li.y * lj.y;
-        g.y -= li.y * lj.x - li.x * lj.y;
-        S[pk(i, j)] = g;
+    const int pn = s_next;  // pivot of step k+1 (n if none)
+    const double2* lk = lvb + (k & 1) * CH_MAXN;
+    if (warp == 0) {
+      if (k + 1 < n && pn < n) {
+        phase_a(k + 1, pn, lk, lvb + ((k + 1) & 1) * CH_MAXN);
+      } else if (k + 1 < n && lane == 0) {  // no pivot left (only for PIVOT): rank k + 1
+        s_brk = 1;
+        s_rank = k + 1;
+      }
+    } else if (!(g_chol_dbg & 1)) {
+      // phase B of step k, rows/columns of p_{k+1} excluded (warp 0 updates that column)
+      for (int i = warp - 1; i < n; i += CH_THREADS / 32 - 1) {
+        if (i == pn || !alive[i]) continue;
+        const double2 li = lk[i];
+        for (int j = lane; j < i; j += 32) {
+          if (j == pn || !alive[j]) continue;
+          const double2 lj = lk[j];
+          double2 g = S[pk(i, j)];
+          g.x -= li.x * lj.x + li.y * lj.y;
+          g.y -= li.y * lj.x - li.x * lj.y;
+          S[pk(i, j)] = g;
+        }
       }
     }
-    (void)p;
     __syncthreads();
   }
   __syncthreads();
