@@ -1,6 +1,7 @@
 // tensor.cu -- device tensors, permutation kernel, FP32 SIMT complex GEMM and the
 // contraction planner (see tensor.h).
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <map>
 
@@ -254,6 +255,56 @@ __device__ __forceinline__ float2 ld_c(const float2* p, bool cj) {
   return v;
 }
 
+// Thin GEMMs (N <= 8, e.g. a physical or unit output leg): one warp per output row, the lanes
+// stride over K (coalesced when A's K stride is 1), N running sums per lane, fixed-order warp
+// reduction. Memory-bound; the tiled SIMT kernel wastes most of its 64-wide N tile here.
+constexpr int THIN_N = 8;
+__global__ void __launch_bounds__(256) cgemm_thin(GemmDesc g) {
+  const int bz = blockIdx.y;
+  const int b1 = bz / g.nb2, b2 = bz - b1 * g.nb2;
+  const float2* A = g.A + b1 * g.sa1 + b2 * g.sa2;
+  const float2* B = g.B + b1 * g.sb1 + b2 * g.sb2;
+  float2* C = g.C + b1 * g.sc1 + b2 * g.sc2;
+  const int lane = threadIdx.x & 31;
+  const int64_t m = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (m >= g.M) return;
+  float2 acc[THIN_N];
+#pragma unroll
+  for (int n = 0; n < THIN_N; ++n) acc[n] = make_float2(0.f, 0.f);
+  for (int k = lane; k < g.K; k += 32) {
+    const float2 a = ld_c(A + m * g.am + (int64_t)k * g.ak, g.conjA);
+#pragma unroll
+    for (int n = 0; n < THIN_N; ++n) {
+      if (n < g.N) {
+        const float2 b = ld_c(B + (int64_t)k * g.bk + (int64_t)n * g.bn, g.conjB);
+        acc[n].x = fmaf(a.x, b.x, fmaf(-a.y, b.y, acc[n].x));
+        acc[n].y = fmaf(a.x, b.y, fmaf(a.y, b.x, acc[n].y));
+      }
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < THIN_N; ++n) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc[n].x += __shfl_xor_sync(0xffffffffu, acc[n].x, o);
+      acc[n].y += __shfl_xor_sync(0xffffffffu, acc[n].y, o);
+    }
+  }
+  if (lane < g.N) {
+    float2 v = acc[0];
+#pragma unroll
+    for (int n = 1; n < THIN_N; ++n)
+      if (lane == n) v = acc[n];
+    float2* cp = C + m * g.cm + lane;
+    if (g.accumulate) {
+      const float2 o = *cp;
+      v.x += o.x;
+      v.y += o.y;
+    }
+    *cp = v;
+  }
+}
+
 __global__ void __launch_bounds__(256) cgemm_simt(GemmDesc g) {
   __shared__ __align__(16) float2 As[BK][BM + PAD];
   __shared__ __align__(16) float2 Bs[BK][BN + PAD];
@@ -347,6 +398,18 @@ __global__ void __launch_bounds__(256) cgemm_simt(GemmDesc g) {
 }
 }  // namespace
 
+// TN_GEMM_LOG: shapes routed to the SIMT GEMM (calls, complex MACs), printed by
+// tn_debug_simt_log() -- instrumentation only.
+static bool simt_log_on() {
+  static int on = -1;
+  if (on < 0) on = getenv("TN_GEMM_LOG") ? 1 : 0;
+  return on == 1;
+}
+std::map<std::string, std::pair<double, double>>& simt_tab() {
+  static auto* t = new std::map<std::string, std::pair<double, double>>();
+  return *t;
+}
+
 bool gemm(Ctx& c, const GemmDesc& g) {
   if (g.M <= 0 || g.N <= 0 || g.nb1 <= 0 || g.nb2 <= 0) return false;
   g_cmacs += (double)g.M * g.N * std::max(g.K, 0) * g.nb1 * g.nb2;
@@ -361,6 +424,13 @@ bool gemm(Ctx& c, const GemmDesc& g) {
     if (c.gemm_mode != 1 && gemm_tc(c, g)) return true;
   }
   ProfScope ps(P_GEMM_SIMT, c.stream);
+  if (simt_log_on()) {
+    char k[128];
+    snprintf(k, sizeof k, "M=%d N=%d K=%d nb1=%d nb2=%d", g.M, g.N, g.K, g.nb1, g.nb2);
+    auto& e = simt_tab()[k];
+    e.first += 1;
+    e.second += (double)g.M * g.N * g.K * g.nb1 * g.nb2;
+  }
   int64_t nbz = (int64_t)g.nb1 * g.nb2;
   if (nbz > 65535) {
     // split the outer batch into chunks
@@ -374,6 +444,12 @@ bool gemm(Ctx& c, const GemmDesc& g) {
       gemm(c, h);
     }
     g_cmacs -= (double)g.M * g.N * g.K * g.nb1 * g.nb2;
+    return false;
+  }
+  if (g.N <= THIN_N && g.K >= 256) {
+    dim3 tgrid(ceil_div(g.M, 8), (unsigned)nbz);
+    cgemm_thin<<<tgrid, 256, 0, c.stream>>>(g);
+    TN_LAUNCHED();
     return false;
   }
   dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, BM), (unsigned)nbz);
@@ -670,3 +746,13 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
 }
 
 }  // namespace tn
+
+extern "C" int tn_debug_simt_log(void) {
+  std::vector<std::pair<double, std::string>> rows;
+  for (auto& kv : tn::simt_tab()) rows.push_back({kv.second.second, kv.first});
+  std::sort(rows.rbegin(), rows.rend());
+  for (size_t i = 0; i < rows.size() && i < 25; ++i)
+    fprintf(stderr, "SIMT %-50s n=%8.0f cmac=%.3e\n", rows[i].second.c_str(), tn::simt_tab()[rows[i].second].first,
+            rows[i].first);
+  return (int)rows.size();
+}

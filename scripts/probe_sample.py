@@ -66,3 +66,4 @@ for nb in batches:
           f"phases ms/step {ph}", flush=True)
 if os.environ.get("TN_GEMM_LOG"):
     LIB.tn_debug_gemm_log()
+    LIB.tn_debug_simt_log()

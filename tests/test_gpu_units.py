@@ -296,3 +296,18 @@ def test_fit_double_matches_oracle():
         ref = _dense(so) * math.exp(lo)
         got = _dense(sg) * math.exp(lg)
         assert np.linalg.norm(got - ref) <= 1e-4 * np.linalg.norm(ref), R
+
+
+@pytest.mark.parametrize("n", [1, 2, 5])
+def test_contract_thin_n(n):
+    """Thin GEMMs (N <= 8, K >= 256) take the warp-per-row kernel: batched, conjugated,
+    strided-K operands against numpy."""
+    rng = np.random.default_rng(12)
+    nb = 3
+    A = rand(rng, (nb, 37, 300))
+    B = rand(rng, (300, n))
+    out, ref = dcontract(A, "mk", B, "kn", "mn", nb=nb, perA=True, cA=True, gemm=1)
+    assert close(out, ref)
+    A2 = rand(rng, (nb, 300, 41))  # K-major A (strided K in the GEMM view)
+    out, ref = dcontract(A2, "km", B, "kn", "nm", nb=nb, perA=True, cB=True, gemm=1)
+    assert close(out, ref)
