@@ -166,12 +166,13 @@ __device__ __forceinline__ float row_amax(const TcParams& p, int z, int row) {
 // Grouped rasterisation: linear tile id -> (m, n), groups of RASTER_GM m-tiles swept with m
 // fastest, so a wave of CTAs shares a few A strips and B strips in L2 instead of streaming
 // one operand strip per CTA from HBM (a full-K strip is 4-8 MB of FP16 planes).
-constexpr int RASTER_GM = 8;
+__device__ int g_raster_gm = 16;  // group height in pair-tiles (4: +2%, 32: +4% step time); tn_debug_raster
 __device__ __forceinline__ void raster(int lin, int nm, int nn, int& m, int& n) {
-  const int per_group = RASTER_GM * nn;
+  const int GM = g_raster_gm;
+  const int per_group = GM * nn;
   const int g = lin / per_group, r = lin - g * per_group;
-  const int m0 = g * RASTER_GM;
-  const int gm = min(RASTER_GM, nm - m0);
+  const int m0 = g * GM;
+  const int gm = min(GM, nm - m0);
   m = m0 + r % gm;
   n = r / gm;
 }
@@ -1231,3 +1232,7 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
 }
 
 }  // namespace tn
+
+extern "C" int tn_debug_raster(int gm) {
+  return cudaMemcpyToSymbol(tn::g_raster_gm, &gm, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
