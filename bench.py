@@ -311,7 +311,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="samples per GPU per step (0 = workload default)")
     ap.add_argument("--order", type=int, default=0, choices=[0, 1],
                     help="0: compress-then-sample (R3, default); 1: the paper's literal order (NEXT-3, R <= chi)")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=40.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
     assert a.warmup >= 1 and a.steps >= 1
