@@ -166,6 +166,7 @@ __device__ __forceinline__ float row_amax(const TcParams& p, int z, int row) {
 // Grouped rasterisation: linear tile id -> (m, n), groups of RASTER_GM m-tiles swept with m
 // fastest, so a wave of CTAs shares a few A strips and B strips in L2 instead of streaming
 // one operand strip per CTA from HBM (a full-K strip is 4-8 MB of FP16 planes).
+__device__ int g_kc = TC_KC;  // k-blocks per promoted chunk in the pair kernel; tn_debug_kc (experiments)
 __device__ int g_raster_gm = 16;  // group height in pair-tiles (4: +2%, 32: +4% step time); tn_debug_raster
 __device__ __forceinline__ void raster(int lin, int nm, int nn, int& m, int& n) {
   const int GM = g_raster_gm;
@@ -505,7 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       for (int t = cluster; t < ntiles; t += nclusters) {
         const PairTile tl = pair_tile(p, t, npm, nn);
         for (int q = 0; q < tl.nkb; ++q, ++i) {
-          const int kin = q % TC_KC, buf = c & 1;
+          const int kin = q % g_kc, buf = c & 1;
           if (kin == 0) {
             mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -526,7 +527,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             mma_f16_pair(dacc, alo + adv, bhi + adv, idesc, 1u);
           }
           mma_commit_pair(&empty[s]);
-          if (kin == TC_KC - 1 || q == tl.nkb - 1) {
+          if (kin == g_kc - 1 || q == tl.nkb - 1) {
             mma_commit_pair(&acc_full[buf]);
             ++c;
           }
@@ -547,7 +548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       float acc[128];
 #pragma unroll
       for (int i = 0; i < 128; ++i) acc[i] = 0.f;
-      const int nchunks = (tl.nkb + TC_KC - 1) / TC_KC;
+      const int nchunks = (tl.nkb + g_kc - 1) / g_kc;
       for (int cc0 = 0; cc0 < nchunks; ++cc0, ++c) {
         const int buf = c & 1;
         mbar_wait(&acc_full[buf], (c >> 1) & 1);
@@ -1235,4 +1236,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
 
 extern "C" int tn_debug_raster(int gm) {
   return cudaMemcpyToSymbol(tn::g_raster_gm, &gm, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
+
+extern "C" int tn_debug_kc(int kc) {
+  return cudaMemcpyToSymbol(tn::g_kc, &kc, sizeof(int)) == cudaSuccess ? 0 : -1;
 }
