@@ -484,11 +484,12 @@ def main():
     tc_ms = prof[6]
     tc_cmacs = cnt[1]
     achieved = (8.0 * tc_cmacs) / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else None
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "tc_gemm_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(a.workload)
+            t = json.load(open(tpath)).get(a.workload)
+            traffic, traffic_src = float(t["bytes_per_launch"]), t["source"]
         except Exception:
             traffic = None
     fp16_peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
@@ -496,6 +497,7 @@ def main():
                 "kernel": "tc_gemm2_kernel / tc_gemm_kernel (tcgen05 kind::f16, CTA pair, FP16x3 split complex GEMM)",
                 "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                 "frac": (achieved / tf32_peak) if achieved else None, "traffic": traffic,
+                "traffic_source": traffic_src,
                 "peak_source": f"{which}: FP32-class tensor peak = bf16_tflops_sustained x 1.1/2.25 (dense TF32/BF16 "
                                f"nominal ratio); the path computes complex64 products to FP32 accuracy",
                 "algorithmic": "8 real flops per complex MAC of the GEMM (M*N*K), counted once (complex as one real "
