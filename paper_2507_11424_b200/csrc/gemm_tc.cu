@@ -770,6 +770,45 @@ __global__ void __launch_bounds__(256) rowmax_kernel(PrepArgs a) {
   }
 }
 
+// rowmax_kernel with the whole 32 x PK_K tile loaded before the scan (see prep_wide_kernel).
+__global__ void __launch_bounds__(256, 4) rowmax_wide_kernel(PrepArgs a) {
+  if (a.zero_me && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *a.zero_me = 0.f;
+  __shared__ float tile[32][PK_K + 1];
+  __shared__ int64_t roff[32], koff[PK_K];
+  __shared__ float part[8][32];
+  const int r0 = blockIdx.x * 32, k0 = blockIdx.y * PK_K, zz = blockIdx.z;  // rows on x (2^31 limit)
+  prep_offsets(a, roff, koff, r0, k0);
+  const float2* base = prep_base(a, zz);
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  float2 v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int rr = a.k_fast ? ty + 8 * (i & 3) : tx;
+    const int kk = a.k_fast ? (i >> 2) * 32 + tx : ty + 8 * i;
+    const int64_t ro = roff[rr], ko = koff[kk];
+    v[i] = make_float2(0.f, 0.f);
+    if (ro >= 0 && ko >= 0) v[i] = base[ro + ko];
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int rr = a.k_fast ? ty + 8 * (i & 3) : tx;
+    const int kk = a.k_fast ? (i >> 2) * 32 + tx : ty + 8 * i;
+    tile[rr][kk] = fmaxf(fabsf(v[i].x), fabsf(v[i].y));
+  }
+  __syncthreads();
+  float m = 0.f;  // warp ty scans 16 k columns of row tx
+#pragma unroll
+  for (int q = 0; q < 16; ++q) m = fmaxf(m, tile[tx][ty * 16 + q]);
+  part[ty][tx] = m;
+  __syncthreads();
+  if (t < 32 && r0 + t < a.R) {
+    float mm = part[0][t];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) mm = fmaxf(mm, part[q][t]);
+    if (mm > 0.f) atomicMax(reinterpret_cast<unsigned int*>(a.mx + (int64_t)zz * a.Rp + r0 + t), __float_as_uint(mm));
+  }
+}
+
 __device__ __forceinline__ void split16(float x, __half& h, __half& l) {
   h = __float2half_rn(x);
   l = __float2half_rn(x - __half2float(h));
@@ -844,6 +883,81 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
   }
 }
 
+// Same planes as prep_tiled_kernel, but the whole 32 x PK_K tile is loaded before any store:
+// 16 independent 8-byte loads per thread in flight instead of 4 per barrier-separated
+// sub-tile (the sub-tile version is memory-latency bound at ~55 % of HBM bandwidth on the
+// large double-layer operands).
+template <int KIND>
+__global__ void __launch_bounds__(256, 4) prep_wide_kernel(PrepArgs a) {
+  __shared__ float2 tile[32][PK_K + 1];
+  __shared__ int64_t roff[32], koff[PK_K];
+  __shared__ float scl[32];
+  const int r0 = blockIdx.x * 32, k0 = blockIdx.y * PK_K, zz = blockIdx.z;  // rows on x
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  if (t >= 224) {
+    const int i = t - 224;
+    const float m = (r0 + i < a.R) ? (a.mx_uniform ? *a.mx_uniform : a.mx[(int64_t)zz * a.Rp + r0 + i]) : 0.f;
+    scl[i] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
+  }
+  prep_offsets(a, roff, koff, r0, k0);
+  const float2* base = prep_base(a, zz);
+  float2 v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int rr = a.k_fast ? ty + 8 * (i & 3) : tx;
+    const int kk = a.k_fast ? (i >> 2) * 32 + tx : ty + 8 * i;
+    const int64_t ro = roff[rr], ko = koff[kk];
+    v[i] = make_float2(0.f, 0.f);
+    if (ro >= 0 && ko >= 0) v[i] = base[ro + ko];
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int rr = a.k_fast ? ty + 8 * (i & 3) : tx;
+    const int kk = a.k_fast ? (i >> 2) * 32 + tx : ty + 8 * i;
+    float2 w = v[i];
+    if (a.conj) w.y = -w.y;
+    tile[rr][kk] = w;
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)a.Rrows * a.Krp;
+  __half2* hi = reinterpret_cast<__half2*>(a.hi + zz * plane);
+  __half2* lo = reinterpret_cast<__half2*>(a.lo + zz * plane);
+  const int kp = a.Krp >> 1;  // half2 per plane row
+#pragma unroll
+  for (int sub = 0; sub < PK_K / 32; ++sub) {
+    const int kc = k0 + sub * 32 + tx;  // complex k of this thread
+    if (2 * kc >= a.Krp) break;
+    if (KIND == 0) {
+#pragma unroll
+      for (int j = ty; j < 32; j += 8) {
+        const int r = r0 + j;
+        if (r >= a.Rrows) continue;
+        const float2 w = tile[j][sub * 32 + tx];
+        const float sc = scl[j];
+        __half2 h, l;
+        split16x2(w.x * sc, w.y * sc, h, l);
+        hi[(int64_t)r * kp + kc] = h;
+        lo[(int64_t)r * kp + kc] = l;
+      }
+    } else {
+#pragma unroll
+      for (int j = ty; j < 32; j += 8) {
+        const int row = 2 * (r0 + j);
+        if (row >= a.Rrows) continue;
+        const float2 b = tile[j][sub * 32 + tx];
+        const float sc = scl[j];
+        __half2 h, l;
+        split16x2(b.x * sc, -b.y * sc, h, l);
+        hi[(int64_t)row * kp + kc] = h;
+        lo[(int64_t)row * kp + kc] = l;
+        split16x2(b.y * sc, b.x * sc, h, l);
+        hi[(int64_t)(row + 1) * kp + kc] = h;
+        lo[(int64_t)(row + 1) * kp + kc] = l;
+      }
+    }
+  }
+}
+
 // A planes when K is the contiguous axis of the operand (innermost K view stride 1, even
 // extent): no shared-memory transpose -- each thread streams 2 consecutive complex k of one
 // row (one 16-byte load) into one half2x2 (8-byte) store per plane, 8 rows per CTA.
@@ -894,6 +1008,12 @@ __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
     hi[(int64_t)r * kq + kpair] = hv;
     lo[(int64_t)r * kq + kpair] = lv;
   }
+}
+
+// TN_PREP_WIDE=0 selects the sub-tile prep kernel (A/B measurement only)
+bool prep_wide_on() {
+  static const bool on = !(getenv("TN_PREP_WIDE") && std::atoi(getenv("TN_PREP_WIDE")) == 0);
+  return on;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1068,10 +1188,12 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     a.hi = bh.as<__half>();
     a.lo = bl.as<__half>();
     dim3 gmax(ceil_div(g.N, 32), ceil_div(g.K, PK_K), nzb);
-    rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
+    if (prep_wide_on()) rowmax_wide_kernel<<<gmax, 256, 0, c.stream>>>(a);
+    else rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
     dim3 grid(Nrp / 64, ceil_div(Krp / 2, PK_K), nzb);
-    prep_tiled_kernel<1><<<grid, 256, 0, c.stream>>>(a);
+    if (prep_wide_on()) prep_wide_kernel<1><<<grid, 256, 0, c.stream>>>(a);
+    else prep_tiled_kernel<1><<<grid, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
   }
   const int bbox = pair ? TC_BN / 2 : TC_BN;
@@ -1130,7 +1252,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       if (!use_uniform) {
         TN_CUDA(cudaMemsetAsync(amx.p, 0, (size_t)nz * Mp * sizeof(float), c.stream));
         dim3 gmax(ceil_div(g.M, 32), ceil_div(g.K, PK_K), nz);
-        rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
+        if (prep_wide_on()) rowmax_wide_kernel<<<gmax, 256, 0, c.stream>>>(a);
+        else rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
         TN_LAUNCHED();
       }
       // K-contiguous operands (innermost K stride 1, even length, 16-byte aligned base and
@@ -1146,7 +1269,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
         prep_kfast_kernel<<<grid, 256, 0, c.stream>>>(a);
       } else {
         dim3 grid(Mp / 32, ceil_div(Krp / 2, PK_K), nz);
-        prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
+        if (prep_wide_on()) prep_wide_kernel<0><<<grid, 256, 0, c.stream>>>(a);
+        else prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
       }
       TN_LAUNCHED();
     }
