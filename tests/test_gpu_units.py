@@ -107,6 +107,21 @@ def test_contract_gather_views(gemm):
     assert close(out, ref)
 
 
+@pytest.mark.parametrize("la,shape", [("kxj", (13, 70, 23)), ("kjx", (13, 23, 70)), ("xjk", (70, 23, 13))])
+def test_contract_prep_ragged_tiles(la, shape):
+    """Tensor-core operand preparation over several 32 x 128 gather tiles with ragged tails in
+    both M (70) and K (13 * 23 = 299), for each contiguity of the A operand (M innermost, K
+    innermost, split K axes), per-sample A and conjugated B."""
+    rng = np.random.default_rng(21)
+    nb = 2
+    A = rand(rng, (nb,) + shape)
+    B = rand(rng, (13, 23, 40))
+    out, ref = dcontract(A, la, B, "kjn", "xn", nb=nb, perA=True, cB=True, gemm=2)
+    assert close(out, ref)
+    out, ref = dcontract(B, "kjn", A, la, "nx", nb=nb, perB=True, cA=True, gemm=2)
+    assert close(out, ref)
+
+
 def test_contract_tiny_rows_tensor_core():
     """Rows/columns of magnitude ~1e-40 (FP32 subnormal) next to O(1) ones: the FP16x3 path's
     power-of-two scaling must stay finite (a scale of 2^139 once overflowed to inf -> NaN)."""
