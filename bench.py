@@ -35,7 +35,7 @@ METRIC = "bitstring samples/sec at 1/2/4/8 B200 (Willow-105, χ_env=128); TC-pip
 # name: lattice, chi, chi_env, samples per GPU per step
 WORKLOADS = {
     # the metric configuration: Willow-105 shapes of config 4 (chi = 32, chi_env = 128)
-    "willow105_chi32_env128": ("willow105", 32, 128, 2),
+    "willow105_chi32_env128": ("willow105", 32, 128, 4),
     # parity / smaller shapes (not the metric)
     "willow105_chi16_env64": ("willow105", 16, 64, 16),
     "willow105_chi8_env32": ("willow105", 8, 32, 256),
