@@ -26,8 +26,10 @@ struct Error : std::runtime_error {
     }                                                                                   \
   } while (0)
 
-// Count of this library's kernel launches (reported as gpu_launches by bench.py).
-extern int64_t g_launches;
+// Count of this library's kernel launches on the calling thread (reported as gpu_launches by
+// bench.py and per call by tn_get_stats). Thread-local: distinct states may be driven from
+// distinct threads concurrently.
+extern thread_local int64_t g_launches;
 inline void note_launch() {
   ++g_launches;
 }
@@ -42,26 +44,32 @@ struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaStream_t s = nullptr;
-  // Optional device float: an upper bound of max |component| over the buffer's complex
-  // contents, written by the tensor-core GEMM that produced them (lets a consumer GEMM scale
-  // its FP16 operand planes without a max pass). It lives in `tail` spare bytes allocated
-  // after the data (no separate allocation); any in-place write must drop it.
+  // Optional device floats: upper bounds of max |component| over the buffer's complex
+  // contents, one per sample of the batch (tail_n = the batch size; 1 for a shared tensor),
+  // written by the tensor-core GEMM that produced them (lets a consumer GEMM scale its FP16
+  // operand planes without a max pass, per sample, so that a sample's result never depends
+  // on which other samples share its batch). They live in `tail` spare bytes allocated after
+  // the data (no separate allocation); any in-place write must drop them.
   float* tail = nullptr;
+  int tail_n = 0;
   bool amax_valid = false;
   DevBuf() = default;
-  DevBuf(size_t n, cudaStream_t st, bool with_tail = false) { alloc(n, st, with_tail); }
-  void alloc(size_t n, cudaStream_t st, bool with_tail = false) {
+  DevBuf(size_t n, cudaStream_t st, int tail_floats = 0) { alloc(n, st, tail_floats); }
+  void alloc(size_t n, cudaStream_t st, int tail_floats = 0) {
     release();
     s = st;
     bytes = n;
     if (n) {
-      const size_t pad = with_tail ? 256 : 0;
+      const size_t pad = tail_floats > 0 ? ((size_t)tail_floats * sizeof(float) + 255) / 256 * 256 : 0;
       TN_CUDA(cudaMallocAsync(&p, n + pad, st));
-      if (with_tail) tail = reinterpret_cast<float*>(reinterpret_cast<char*>(p) + ((n + 15) / 16) * 16);
+      if (tail_floats > 0) {
+        tail = reinterpret_cast<float*>(reinterpret_cast<char*>(p) + ((n + 15) / 16) * 16);
+        tail_n = tail_floats;
+      }
     }
   }
   float* amax() const { return amax_valid ? tail : nullptr; }
-  float* make_amax() {  // the producing GEMM zeroes it (stream order) before writing
+  float* make_amax() {  // the producer zeroes the tail_n floats (stream order) before writing
     if (!tail) return nullptr;
     amax_valid = true;
     return tail;
@@ -71,20 +79,22 @@ struct DevBuf {
     if (p) cudaFreeAsync(p, s);
     p = nullptr;
     tail = nullptr;
+    tail_n = 0;
     amax_valid = false;
     bytes = 0;
   }
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s), tail(o.tail), amax_valid(o.amax_valid) {
-    o.p = nullptr; o.bytes = 0; o.tail = nullptr; o.amax_valid = false;
+  DevBuf(DevBuf&& o) noexcept
+      : p(o.p), bytes(o.bytes), s(o.s), tail(o.tail), tail_n(o.tail_n), amax_valid(o.amax_valid) {
+    o.p = nullptr; o.bytes = 0; o.tail = nullptr; o.tail_n = 0; o.amax_valid = false;
   }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; bytes = o.bytes; s = o.s; tail = o.tail; amax_valid = o.amax_valid;
-      o.p = nullptr; o.bytes = 0; o.tail = nullptr; o.amax_valid = false;
+      p = o.p; bytes = o.bytes; s = o.s; tail = o.tail; tail_n = o.tail_n; amax_valid = o.amax_valid;
+      o.p = nullptr; o.bytes = 0; o.tail = nullptr; o.tail_n = 0; o.amax_valid = false;
     }
     return *this;
   }

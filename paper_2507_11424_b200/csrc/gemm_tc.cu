@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -66,9 +67,20 @@ struct TcParams {
   int64_t sc1, sc2;
   int z0;
   int accumulate;
-  const float* amax_uniform;  // non-null: one scale for all rows of A (max over the tensor)
-  float* amax_out;            // non-null: atomicMax of max |component| of the stored C values
+  const float* amax_sample;   // non-null: one scale per sample for the rows of A (producer's bound)
+  int amax_sample_n;          // its count (1: one bound for every row)
+  float* amax_out;            // non-null: atomicMax of max |component| of the stored C values, per sample
+  int amax_out_n;             // its count
+  int rows_per_sample;        // > 0: sample of row m = m / rows_per_sample (batch folded into M);
+                              // 0: sample = (z0 + z) / nb2 (outer batch index)
 };
+
+// Sample of an M-side row (A's rows and C's rows share the mapping), for bounds of count n.
+__device__ __forceinline__ int sample_of(int rows_per_sample, int z0, int z, int nb2, int row, int n) {
+  if (n <= 1) return 0;
+  const int s = rows_per_sample > 0 ? row / rows_per_sample : (z0 + z) / nb2;
+  return min(s, n - 1);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -160,7 +172,21 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 __device__ __forceinline__ float row_amax(const TcParams& p, int z, int row) {
-  return p.amax_uniform ? *p.amax_uniform : p.amax[(int64_t)z * p.Mp + row];
+  if (p.amax_sample) return p.amax_sample[sample_of(p.rows_per_sample, p.z0, z, p.nb2, row, p.amax_sample_n)];
+  return p.amax[(int64_t)z * p.Mp + row];
+}
+
+// Per-sample output bound of a warp whose lanes hold rows rows0..rows0+31 (1-CTA kernel: lane =
+// row): one atomic when the warp's rows belong to one sample, else one per lane.
+__device__ __forceinline__ void amax_out_rows(const TcParams& p, int z, int row, float lmax) {
+  const int s = sample_of(p.rows_per_sample, p.z0, z, p.nb2, row, p.amax_out_n);
+  const int s0 = __shfl_sync(0xffffffffu, s, 0);
+  if (__all_sync(0xffffffffu, s == s0)) {
+    lmax = warp_max(lmax);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(p.amax_out + s0, lmax);
+  } else {
+    atomic_max_nonneg(p.amax_out + s, lmax);
+  }
 }
 
 // Grouped rasterisation: linear tile id -> (m, n), groups of RASTER_GM m-tiles swept with m
@@ -333,10 +359,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
-    if (p.amax_out && p.ksplit == 1) {
-      lmax = warp_max(lmax);
-      if (lane == 0) atomic_max_nonneg(p.amax_out, lmax);
-    }
+    if (p.amax_out && p.ksplit == 1) amax_out_rows(p, z, row, lmax);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -602,6 +625,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         }
         __syncwarp();
         const int sub = lane >> 3, col = lane & 7;
+        // per-sample output bounds: one per warp when its 32 rows belong to one sample (always,
+        // unless a sample's row count is not a multiple of 32), else one atomic per element
+        const int s_lo = sample_of(p.rows_per_sample, p.z0, z, p.nb2, row0, p.amax_out_n);
+        const bool s_mixed = p.amax_out && p.ksplit == 1 &&
+                             sample_of(p.rows_per_sample, p.z0, z, p.nb2, min(row0 + 31, p.M - 1), p.amax_out_n) != s_lo;
 #pragma unroll
         for (int q0 = 0; q0 < 64; q0 += EPI_Q) {
 #pragma unroll
@@ -623,14 +651,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                 val.y += o.y;
               }
               *dst = val;
-              lmax = fmaxf(lmax, fmaxf(fabsf(val.x), fabsf(val.y)));
+              const float mv = fmaxf(fabsf(val.x), fabsf(val.y));
+              if (s_mixed)
+                atomic_max_nonneg(p.amax_out + sample_of(p.rows_per_sample, p.z0, z, p.nb2, grow, p.amax_out_n), mv);
+              lmax = fmaxf(lmax, mv);
             }
           }
           __syncwarp();
         }
-        if (p.amax_out && p.ksplit == 1) {
+        if (p.amax_out && p.ksplit == 1 && !s_mixed) {
           lmax = warp_max(lmax);
-          if (lane == 0) atomic_max_nonneg(p.amax_out, lmax);
+          if (lane == 0) atomic_max_nonneg(p.amax_out + s_lo, lmax);
         }
       }
     }
@@ -645,7 +676,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 // Deterministic split-K reduction: C (+)= sum over splits in a fixed order.
 __global__ void splitk_reduce_kernel(const float2* __restrict__ ws, int ksplit, int64_t ws_split, int nz, int M,
                                      int N, float2* C, int64_t cm, int nb2, int64_t sc1, int64_t sc2, int z0,
-                                     int accumulate, float* amax_out) {
+                                     int accumulate, float* amax_out, int amax_out_n, int rows_per_sample) {
   const int64_t per = (int64_t)M * N, tot = per * nz;
   float lmax = 0.f;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
@@ -666,9 +697,12 @@ __global__ void splitk_reduce_kernel(const float2* __restrict__ ws, int ksplit, 
       s.y += o.y;
     }
     *cp = s;
-    lmax = fmaxf(lmax, fmaxf(fabsf(s.x), fabsf(s.y)));
+    const float mv = fmaxf(fabsf(s.x), fabsf(s.y));
+    if (amax_out && amax_out_n > 1)
+      atomic_max_nonneg(amax_out + sample_of(rows_per_sample, z0, (int)zz, nb2, row, amax_out_n), mv);
+    lmax = fmaxf(lmax, mv);
   }
-  if (amax_out) {
+  if (amax_out && amax_out_n <= 1) {
     lmax = warp_max(lmax);
     if ((threadIdx.x & 31) == 0) atomic_max_nonneg(amax_out, lmax);
   }
@@ -698,8 +732,9 @@ struct PrepArgs {
   int z0, R, K, Rrows, Krp;  // Rrows: padded plane rows (A: Mp; B: Nrp)
   int k_fast;
   float* mx;                 // [z][Rp] row maxima (max pass writes, prep reads)
-  const float* mx_uniform;   // non-null: one maximum for every row (no max pass)
-  float* zero_me;            // non-null: set to 0 by block (0,0,0) (the GEMM's output maximum)
+  const float* mx_sample;    // non-null: one maximum per sample for its rows (no max pass)
+  int mx_sample_n;           // count of mx_sample (1: one maximum for every row)
+  int rows_per_sample;       // sample of row r: r / rows_per_sample, or (z0 + z) / nb2 when 0
   int Rp;                    // row count of mx per z (complex rows)
   __half* hi;
   __half* lo;
@@ -731,6 +766,11 @@ __device__ __forceinline__ void load_sub(const PrepArgs& a, const float2* base, 
   }
 }
 
+__device__ __forceinline__ float prep_rowmax(const PrepArgs& a, int zz, int r) {
+  if (a.mx_sample) return a.mx_sample[sample_of(a.rows_per_sample, a.z0, zz, a.nb2, r, a.mx_sample_n)];
+  return a.mx[(int64_t)zz * a.Rp + r];
+}
+
 __device__ __forceinline__ const float2* prep_base(const PrepArgs& a, int zz) {
   const int z = a.z0 + zz;
   const int b1 = z / a.nb2, b2 = z - b1 * a.nb2;
@@ -740,7 +780,6 @@ __device__ __forceinline__ const float2* prep_base(const PrepArgs& a, int zz) {
 // Pass 1: max |component| of every row over K (atomicMax on the IEEE bits of a non-negative
 // float is order-independent, hence deterministic).
 __global__ void __launch_bounds__(256) rowmax_kernel(PrepArgs a) {
-  if (a.zero_me && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *a.zero_me = 0.f;
   __shared__ float2 tile[32][33];
   __shared__ int64_t roff[32], koff[PK_K];
   const int r0 = blockIdx.x * 32, k0 = blockIdx.y * PK_K, zz = blockIdx.z;  // rows on x (2^31 limit)
@@ -772,7 +811,6 @@ __global__ void __launch_bounds__(256) rowmax_kernel(PrepArgs a) {
 
 // rowmax_kernel with the whole 32 x PK_K tile loaded before the scan (see prep_wide_kernel).
 __global__ void __launch_bounds__(256, 4) rowmax_wide_kernel(PrepArgs a) {
-  if (a.zero_me && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *a.zero_me = 0.f;
   __shared__ float tile[32][PK_K + 1];
   __shared__ int64_t roff[32], koff[PK_K];
   __shared__ float part[8][32];
@@ -834,7 +872,7 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
   if (t >= 224) {
     const int i = t - 224;
-    const float m = (r0 + i < a.R) ? (a.mx_uniform ? *a.mx_uniform : a.mx[(int64_t)zz * a.Rp + r0 + i]) : 0.f;
+    const float m = (r0 + i < a.R) ? prep_rowmax(a, zz, r0 + i) : 0.f;
     scl[i] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
   }
   prep_offsets(a, roff, koff, r0, k0);
@@ -896,7 +934,7 @@ __global__ void __launch_bounds__(256, 4) prep_wide_kernel(PrepArgs a) {
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
   if (t >= 224) {
     const int i = t - 224;
-    const float m = (r0 + i < a.R) ? (a.mx_uniform ? *a.mx_uniform : a.mx[(int64_t)zz * a.Rp + r0 + i]) : 0.f;
+    const float m = (r0 + i < a.R) ? prep_rowmax(a, zz, r0 + i) : 0.f;
     scl[i] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
   }
   prep_offsets(a, roff, koff, r0, k0);
@@ -971,7 +1009,7 @@ __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
   if (t < PKF_ROWS) {
     const int r = r0 + t;
     roff[t] = (r < a.R) ? view_off(a.vr, r) : -1;
-    const float m = (r < a.R) ? (a.mx_uniform ? *a.mx_uniform : a.mx[(int64_t)zz * a.Rp + r]) : 0.f;
+    const float m = (r < a.R) ? prep_rowmax(a, zz, r) : 0.f;
     scl[t] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
   }
   const int kpair = blockIdx.y * PKF_PAIRS + t;  // complex k = 2 kpair, 2 kpair + 1
@@ -1102,6 +1140,8 @@ extern "C" int tn_debug_gemm_log(void) {
 
 namespace tn {
 
+int g_zc_max = 0;  // > 0: at most this many batch elements per A-plane chunk (tn_debug_set_zc)
+
 bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per_sample) {
   if (c.gemm_mode == 1) return false;
   if (M <= 0 || N <= 0 || K <= 0) return false;
@@ -1138,11 +1178,15 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       }
     }
   } slog_end{slog, srec, c.stream};
-  static bool attr = false;
-  if (!attr) {
+  // kernel attributes are per device context: set once per device ordinal
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  TN_CUDA(cudaGetDevice(&dev));
+  const uint64_t dbit = 1ull << (dev & 63);
+  if (!(attr_done.load() & dbit)) {
     TN_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     TN_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
-    attr = true;
+    attr_done.fetch_or(dbit);
   }
   // CTA pairs (M = 256 per cluster) whenever one batch element has more than 128 rows
   static const bool pair_off = getenv("TN_TC2") && std::atoi(getenv("TN_TC2")) == 0;
@@ -1166,7 +1210,10 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
   DevBuf bh((size_t)nzb * Nrp * Krp * 2, c.stream), bl((size_t)nzb * Nrp * Krp * 2, c.stream);
   DevBuf bmx((size_t)nzb * Np * sizeof(float), c.stream);
   TN_CUDA(cudaMemsetAsync(bmx.p, 0, (size_t)nzb * Np * sizeof(float), c.stream));
-  {
+  if (g.amaxC) TN_CUDA(cudaMemsetAsync(g.amaxC, 0, sizeof(float) * std::max(1, g.amaxC_n), c.stream));
+  // grid.z <= 65535: per-sample B planes are prepared in chunks of batch elements
+  for (int zb0 = 0; zb0 < nzb; zb0 += 65535) {
+    const int nzc = std::min(65535, nzb - zb0);
     PrepArgs a;
     a.X = g.B;
     a.vr = g.vbn.rank ? g.vbn : simple(g.N, g.bn);
@@ -1175,23 +1222,24 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     a.nb2 = g.nb2;
     a.s1 = b_batched ? g.sb1 : 0;
     a.s2 = b_batched ? g.sb2 : 0;
-    a.z0 = 0;
+    a.z0 = zb0;
     a.R = g.N;
     a.K = g.K;
     a.Rrows = Nrp;
     a.Krp = Krp;
     a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
-    a.mx = bmx.as<float>();
-    a.mx_uniform = nullptr;
-    a.zero_me = g.amaxC;
+    a.mx = bmx.as<float>() + (int64_t)zb0 * Np;
+    a.mx_sample = nullptr;
+    a.mx_sample_n = 0;
+    a.rows_per_sample = 0;
     a.Rp = Np;
-    a.hi = bh.as<__half>();
-    a.lo = bl.as<__half>();
-    dim3 gmax(ceil_div(g.N, 32), ceil_div(g.K, PK_K), nzb);
+    a.hi = bh.as<__half>() + (int64_t)zb0 * Nrp * Krp;
+    a.lo = bl.as<__half>() + (int64_t)zb0 * Nrp * Krp;
+    dim3 gmax(ceil_div(g.N, 32), ceil_div(g.K, PK_K), nzc);
     if (prep_wide_on()) rowmax_wide_kernel<<<gmax, 256, 0, c.stream>>>(a);
     else rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
-    dim3 grid(Nrp / 64, ceil_div(Krp / 2, PK_K), nzb);
+    dim3 grid(Nrp / 64, ceil_div(Krp / 2, PK_K), nzc);
     if (prep_wide_on()) prep_wide_kernel<1><<<grid, 256, 0, c.stream>>>(a);
     else prep_tiled_kernel<1><<<grid, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
@@ -1213,14 +1261,17 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     kbps = ((kblocks + ksplit - 1) / ksplit + TC_KC - 1) / TC_KC * TC_KC;
     ksplit = (kblocks + kbps - 1) / kbps;
   }
-  // A's scale: one exponent for the whole operand when its producer recorded max |component|
-  // (no row-max pass; error per element <= 2^-24 of that maximum), else per row.
+  // A's scale: one exponent per sample when its producer recorded the sample's max |component|
+  // (no row-max pass; error per element <= 2^-24 of that maximum), else per row. Rows map to
+  // samples as row / m_per_sample when the batch is folded into M, else by the outer batch index.
   static const bool uniform_off = getenv("TN_ROWSCALE") && std::atoi(getenv("TN_ROWSCALE")) != 0;
   const bool use_uniform = g.amaxA != nullptr && !uniform_off;
+  const int rows_per_sample = g.nb1 > 1 ? 0 : (g.m_per_sample > 0 ? g.m_per_sample : g.M);
   // ---- A planes, chunked over the batch to bound the workspace (<= ~1 GB per plane)
   const int64_t per_z = (int64_t)Mp * Krp;
-  const int zc = (int)std::max<int64_t>(
+  const int zc0 = (int)std::max<int64_t>(
       1, std::min<int64_t>({(int64_t)nbz, (int64_t)(65535 / ksplit), (int64_t)(1ll << 29) / std::max<int64_t>(1, per_z)}));
+  const int zc = g_zc_max > 0 ? std::min(zc0, g_zc_max) : zc0;  // tn_debug_set_zc: force chunking (tests)
   DevBuf ah((size_t)zc * per_z * 2, c.stream), al((size_t)zc * per_z * 2, c.stream);
   DevBuf amx((size_t)zc * Mp * sizeof(float), c.stream);
   DevBuf ws;
@@ -1244,8 +1295,9 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       a.Krp = Krp;
       a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
       a.mx = amx.as<float>();
-      a.mx_uniform = use_uniform ? g.amaxA : nullptr;
-      a.zero_me = nullptr;
+      a.mx_sample = use_uniform ? g.amaxA : nullptr;
+      a.mx_sample_n = std::max(1, g.amaxA_n);
+      a.rows_per_sample = rows_per_sample;
       a.Rp = Mp;
       a.hi = ah.as<__half>();
       a.lo = al.as<__half>();
@@ -1296,8 +1348,11 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.sc2 = g.sc2;
     p.z0 = z0;
     p.accumulate = g.accumulate ? 1 : 0;
-    p.amax_uniform = use_uniform ? g.amaxA : nullptr;
+    p.amax_sample = use_uniform ? g.amaxA : nullptr;
+    p.amax_sample_n = std::max(1, g.amaxA_n);
     p.amax_out = g.amaxC;
+    p.amax_out_n = std::max(1, g.amaxC_n);
+    p.rows_per_sample = rows_per_sample;
     if (slog && z0 == 0) cudaEventRecord(srec.b, c.stream);
     {
       ProfScope ps(P_TC_KERNEL, c.stream);
@@ -1312,7 +1367,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
         // persistent CTA pairs over all (z, split, m pair, n) tiles
         const int npm = Mp / (2 * TC_BM), nn = Nrp / TC_BN;
         const int ntiles = nz * ksplit * npm * nn;
-        static int max_clusters = 0;
+        static std::atomic<int> max_clusters_dev[64];
+        int max_clusters = max_clusters_dev[dev & 63].load();
         if (!max_clusters) {
           // clusters that can be co-resident (a persistent grid larger than this would run
           // its surplus clusters as a serial second wave)
@@ -1333,6 +1389,7 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
             n = 64;
           }
           max_clusters = std::min(n, 74);
+          max_clusters_dev[dev & 63].store(max_clusters);
           if (getenv("TN_GEMM_LOG")) fprintf(stderr, "tc_gemm2: %d co-resident CTA pairs\n", max_clusters);
         }
         static const bool persist = !(getenv("TN_PERSIST") && std::atoi(getenv("TN_PERSIST")) == 0);
@@ -1349,7 +1406,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       int64_t tot = (int64_t)nz * g.M * g.N;
       unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16);
       splitk_reduce_kernel<<<blocks, 256, 0, c.stream>>>(p.ws, ksplit, ws_split, nz, g.M, g.N, g.C, g.cm, g.nb2,
-                                                         g.sc1, g.sc2, z0, p.accumulate, g.amaxC);
+                                                         g.sc1, g.sc2, z0, p.accumulate, g.amaxC, p.amax_out_n,
+                                                         rows_per_sample);
       TN_LAUNCHED();
     }
   }
@@ -1360,6 +1418,11 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
 
 extern "C" int tn_debug_raster(int gm) {
   return cudaMemcpyToSymbol(tn::g_raster_gm, &gm, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
+
+extern "C" int tn_debug_set_zc(int zc) {
+  tn::g_zc_max = zc;
+  return 0;
 }
 
 extern "C" int tn_debug_kc(int kc) {

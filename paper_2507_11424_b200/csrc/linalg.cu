@@ -1,5 +1,6 @@
 // linalg.cu -- CholeskyQR2 with pivoted rank detection, FP64 arithmetic (see linalg.h).
 #include <algorithm>
+#include <atomic>
 #include <complex>
 #include <cstdio>
 #include <vector>
@@ -843,11 +844,15 @@ static void gram(Ctx& c, const MatView& Y, const MatView& X, int m, int nb, bool
 
 static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, int nb) {
   const int m = X.m, n = X.n;
-  static bool attr = false;
-  if (!attr) {
+  // kernel attributes are per device context: set once per device ordinal
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  TN_CUDA(cudaGetDevice(&dev));
+  const uint64_t dbit = 1ull << (dev & 63);
+  if (!(attr_done.load() & dbit)) {
     TN_CUDA(cudaFuncSetAttribute(chol_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CH_SMEM));
     TN_CUDA(cudaFuncSetAttribute(chol_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CH_SMEM));
-    attr = true;
+    attr_done.fetch_or(dbit);
   }
   static const double tol = getenv("TN_ORTH_TOL") ? atof(getenv("TN_ORTH_TOL")) : 1e-13;
   static const bool always2 = getenv_flag("TN_ORTH_ALWAYS2");

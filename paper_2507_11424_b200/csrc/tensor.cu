@@ -9,11 +9,11 @@
 
 namespace tn {
 
-int64_t g_launches = 0;
-double g_cmacs = 0.0;
-double g_cmacs_tc = 0.0;
-int64_t g_tc_launches = 0;
-std::vector<double> g_row_cmacs;
+thread_local int64_t g_launches = 0;
+thread_local double g_cmacs = 0.0;
+thread_local double g_cmacs_tc = 0.0;
+thread_local int64_t g_tc_launches = 0;
+thread_local std::vector<double> g_row_cmacs;
 
 // tcgen05 path (gemm_tc.cu); returns false when the shape/layout is not eligible.
 bool gemm_tc(Ctx& c, const GemmDesc& g);
@@ -24,7 +24,7 @@ Tensor new_tensor_n(Ctx& c, const std::vector<int>& shape, int nb) {
   int64_t sz = prod(shape);
   t.bstride = nb > 1 ? sz : (nb == 1 ? sz : 0);
   size_t bytes = (size_t)std::max<int64_t>(1, sz * std::max(nb, 1)) * sizeof(float2);
-  t.mem = std::make_shared<DevBuf>(bytes, c.stream, true);
+  t.mem = std::make_shared<DevBuf>(bytes, c.stream, std::max(nb, 1));
   t.p = t.mem->as<float2>();
   return t;
 }
@@ -723,8 +723,14 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
     g.nb1 = 1;
   }
   // operand / output magnitude bounds (tensor-core path): A's bound spares its row-max pass
-  if (Xu == &X) g.amaxA = tensor_amax(X);
-  if (C.mem && !g.accumulate) g.amaxC = C.mem->make_amax();
+  if (Xu == &X) {
+    g.amaxA = tensor_amax(X, &g.amaxA_n);
+    if (g.amaxA_n < (X.bstride ? c.nb : 1)) g.amaxA = nullptr;  // bounds of another batch
+  }
+  if (C.mem && !g.accumulate) {
+    g.amaxC = C.mem->make_amax();
+    g.amaxC_n = C.mem->tail_n;
+  }
   const bool tc = gemm(c, g);
   if (!tc && C.mem) C.mem->drop_amax();
   if (direct) return C;
@@ -738,8 +744,9 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
   for (char ch : src) Ct.shape.push_back(dim.count(ch) ? dim[ch] : 1);
   if (gl == "?") { Ct.shape = oshape; return Ct; }
   Tensor R = permute(c, Ct, src.c_str(), dst.c_str(), false);
-  if (C.mem && C.mem->amax() && R.mem && R.mem->tail) {  // same values, new layout
-    TN_CUDA(cudaMemcpyAsync(R.mem->tail, C.mem->tail, sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+  if (C.mem && C.mem->amax() && R.mem && R.mem->tail && R.mem->tail_n >= C.mem->tail_n) {  // same values
+    TN_CUDA(cudaMemcpyAsync(R.mem->tail, C.mem->tail, sizeof(float) * C.mem->tail_n, cudaMemcpyDeviceToDevice,
+                            c.stream));
     R.mem->make_amax();
   }
   return R;

@@ -25,9 +25,13 @@ struct Tensor {
   int rank() const { return (int)shape.size(); }
 };
 
-// max |component| bound of a tensor's memory (nullptr if unknown) and its invalidation, to be
-// called by every in-place write (see DevBuf::amax).
-inline const float* tensor_amax(const Tensor& t) { return t.mem ? t.mem->amax() : nullptr; }
+// max |component| bounds of a tensor's memory, one per sample (nullptr if unknown; *n = their
+// count: the batch size of a per-sample tensor, 1 for a shared one), and their invalidation,
+// to be called by every in-place write (see DevBuf::amax).
+inline const float* tensor_amax(const Tensor& t, int* n = nullptr) {
+  if (n) *n = t.mem ? t.mem->tail_n : 0;
+  return t.mem ? t.mem->amax() : nullptr;
+}
 inline void invalidate_amax(const Tensor& t) {
   if (t.mem) t.mem->drop_amax();
 }
@@ -79,8 +83,12 @@ struct GemmDesc {
   bool accumulate = false;
   int64_t work_per_sample = 0;  // complex MACs of one sample (kernel choice must not depend on batch)
   int m_per_sample = 0;         // M before the sample batch was folded into it
-  const float* amaxA = nullptr;  // max |component| bound of all of A (skips A's row-max pass)
-  float* amaxC = nullptr;        // if set: receives max |component| of C (tensor-core path only)
+  // Per-sample max |component| bounds (the sample of an M-side row is row / m_per_sample when
+  // the batch is folded into M, else the outer batch index b1; a count of 1 = one bound for all).
+  const float* amaxA = nullptr;  // bounds of A (skip A's row-max pass)
+  int amaxA_n = 0;
+  float* amaxC = nullptr;        // if set: receives the bounds of C (tensor-core path only)
+  int amaxC_n = 0;
 };
 // Returns true when the tensor-core path ran (and filled g.amaxC if set).
 bool gemm(Ctx& c, const GemmDesc& g);
@@ -88,9 +96,10 @@ bool gemm(Ctx& c, const GemmDesc& g);
 bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per_sample);
 
 // Flop accounting of the GEMMs issued (complex MACs), for the roofline report.
-extern double g_cmacs;
-extern double g_cmacs_tc;      // the part issued to the tcgen05 kernel
-extern int64_t g_tc_launches;  // tcgen05 GEMM kernel launches
-extern std::vector<double> g_row_cmacs;  // per-row complex MACs of the last sampled batch
+// Thread-local (see g_launches).
+extern thread_local double g_cmacs;
+extern thread_local double g_cmacs_tc;      // the part issued to the tcgen05 kernel
+extern thread_local int64_t g_tc_launches;  // tcgen05 GEMM kernel launches
+extern thread_local std::vector<double> g_row_cmacs;  // per-row complex MACs of the last sampled batch
 
 }  // namespace tn

@@ -628,6 +628,15 @@ void sample_common(tn_state* st, const int32_t* row_ptr, const int32_t* rv, int3
     throw;
   }
   st->ctx.stream = saved;
+  if (user_stream && user_stream != st->stream) {
+    // the library frees its cached buffers (environments, layouts) on st->stream: order those
+    // frees after the kernels just queued on the caller's stream
+    cudaEvent_t ev;
+    TN_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TN_CUDA(cudaEventRecord(ev, user_stream));
+    TN_CUDA(cudaStreamWaitEvent(st->stream, ev, 0));
+    TN_CUDA(cudaEventDestroy(ev));
+  }
   st->last_launches = g_launches - l0;
 }
 

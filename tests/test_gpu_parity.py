@@ -131,6 +131,29 @@ def test_branch_superposition_willow_full_chi():
         assert abs(logq[k] - sum(math.log(r) for r in ref)) <= 1e-4 * max(1, abs(logq[k]))
 
 
+def test_branch_superposition_metric_shapes_exact():
+    """Exact regime at the METRIC shapes (chi = 32, chi_env = 128): K = 11 branches on three
+    full-width Willow-105 rows (widths 3, 5, 7) give single-layer boundary ranks <= 11 and
+    double-layer ranks <= 121 <= chi_env, so the method is exact while every
+    fit runs at D = 128 with rank-deficient completion (R7), the ladder GEMMs have the
+    metric shapes (Y2 = Y1 M_j: M = 2R^2 per sample, K = N = chi R = 4096; the per-sample-B
+    contractions batch-chunked) and K = 8192 real reductions use the 8-chunk promotion.
+    Every conditional and ln q is compared with the closed form of the branch sum
+    (maths, not the oracle), element-wise at R16."""
+    from tests.test_oracle import closed_form_conditionals
+    lat = L.row_strip(L.willow105(), 1, 4)
+    st = S.branch_superposition(lat, 32, 11, seed=23)
+    u = S.uniforms(3, lat.n, 29)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 128, u)
+    order = order_of(lat.rows)
+    assert (flags == 0).all()
+    for k in range(len(u)):
+        ref = closed_form_conditionals(st["meta"]["phis"], order, bits[k])
+        for v, r in zip(order, ref):
+            assert abs(cond[k, v] - r) <= 1e-4 * r + (1e-6 if r < 1e-2 else 0), (k, v, cond[k, v], r)
+        assert abs(logq[k] - sum(math.log(r) for r in ref)) <= 1e-4 * max(1, abs(logq[k]))
+
+
 def test_ghz_eagle():
     lat = L.eagle127()
     st = S.ghz(lat, chi=2)
@@ -166,6 +189,31 @@ def test_batch_size_determinism():
     g.set_option("max_batch", 7)
     b2, l2, _, _ = g.sample(lat.rows, 16, u)
     assert (b1 == b2).all() and np.array_equal(l1, l2)
+
+
+@pytest.mark.parametrize("gemm", [2, 0])
+def test_batch_size_determinism_tensor_cores(gemm):
+    """Results of a sample do not depend on which other samples share its batch (header:
+    "results do not depend on batching or GPU count"): the tensor-core path (gemm = 2 forces
+    it for every GEMM) scales produced operands per sample, so bits, ln q and every
+    conditional are bitwise identical for max_batch in {1, 3, all}, on heterogeneous samples
+    (config 2 quench state at finite chi_env, different branches per sample)."""
+    lat, st = G.config_state("cfg2")
+    u = S.uniforms(7, lat.n, 4)
+    u[3] = 0.999  # an extreme sample in the middle of the batch
+    g = TNState(st)
+    g.set_option("gemm", gemm)
+    ref = g.sample(lat.rows, 16, u, want_cond=True)
+    for mb in (1, 3):
+        g.set_option("max_batch", mb)
+        got = g.sample(lat.rows, 16, u, want_cond=True)
+        assert (got[0] == ref[0]).all(), mb
+        assert np.array_equal(got[1], ref[1]), mb
+        assert np.array_equal(got[2], ref[2]), mb
+    # a sample alone equals the same sample inside a batch
+    g.set_option("max_batch", 0)
+    one = g.sample(lat.rows, 16, u[5:6], want_cond=True)
+    assert (one[0][0] == ref[0][5]).all() and one[1][0] == ref[1][5]
 
 
 def test_certify_matches_oracle_metrics():

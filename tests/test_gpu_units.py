@@ -326,3 +326,75 @@ def test_contract_thin_n(n):
     A2 = rand(rng, (nb, 300, 41))  # K-major A (strided K in the GEMM view)
     out, ref = dcontract(A2, "km", B, "kn", "nm", nb=nb, perA=True, cB=True, gemm=1)
     assert close(out, ref)
+
+
+# ---------------------------------------------------------------- metric-shape GEMMs
+LIB.tn_debug_set_zc.argtypes = [C.c_int]
+
+
+def _contract_only(A, la, B, lb, lout, out_shape, nb, perA, perB, gemm=0):
+    """GPU contraction without a full reference (large shapes)."""
+    shA = A.shape[1:] if perA else A.shape
+    shB = B.shape[1:] if perB else B.shape
+    out = np.zeros(out_shape, dtype=np.complex64)
+    sa = (C.c_int * len(shA))(*shA)
+    sb = (C.c_int * len(shB))(*shB)
+    rc = LIB.tn_debug_contract(la.encode(), len(shA), sa, A.ctypes.data_as(C.c_void_p), 0, int(perA),
+                               lb.encode(), len(shB), sb, B.ctypes.data_as(C.c_void_p), 0, int(perB),
+                               lout.encode(), nb, out.ctypes.data_as(C.c_void_p), C.c_int64(out.size), gemm)
+    assert rc == 0, LIB.tn_debug_last_error()
+    return out
+
+
+def _rand32(rng, shape):
+    a = np.empty(shape, dtype=np.complex64)
+    a.real = rng.standard_normal(shape, dtype=np.float32)
+    a.imag = rng.standard_normal(shape, dtype=np.float32)
+    return a
+
+
+def test_gemm_ladder_shape_elementwise():
+    """The dominant ladder GEMM at the metric shape (Y2 = Y1 . M_j: per sample
+    M = 2R^2 = 32768, K = N = chi R = 4096, two samples folded into M = 65536, shared B), on
+    the tcgen05 FP16x3 path, element-wise against an FP64 reference on sampled rows of both
+    samples: max |dC| <= 1e-5 max |C_ref| per row (FP32-class accuracy of R24; K = 8192 real
+    reduction through the chunk promotion). Rows carry magnitudes over 6 decades and the two
+    samples differ by 1e3 (per-row / per-sample scaling)."""
+    rng = np.random.default_rng(41)
+    nb, M, K, N = 2, 32768, 4096, 4096
+    A = _rand32(rng, (nb, M, K))
+    A *= (10.0 ** rng.uniform(-6, 0, (nb, M, 1))).astype(np.float32)
+    A[1] *= np.float32(1e-3)
+    B = (_rand32(rng, (K, N)) / np.float32(64.0)).astype(np.complex64)
+    out = _contract_only(A, "mk", B, "kn", "mn", (nb, M, N), nb, True, False, gemm=2)
+    rows = rng.choice(M, 48, replace=False)
+    Bd = B.astype(np.complex128)
+    for q in range(nb):
+        ref = A[q, rows].astype(np.complex128) @ Bd
+        err = np.abs(out[q, rows] - ref).max(axis=1) / np.abs(ref).max(axis=1)
+        print("ladder shape max elementwise rel err", q, err.max()); assert err.max() <= 1e-5, (q, err.max())
+    assert np.isfinite(out).all()
+
+
+@pytest.mark.parametrize("zc", [0, 2, 1])
+def test_gemm_per_sample_b_chunked(zc):
+    """Contraction with per-sample B over a batched label (the N = 128 ladder closure Rs =
+    Y2 . conj(n): M = R^2, K = chi R = 4096, batched over s and the samples):
+    A planes built in chunks of zc batch elements (tn_debug_set_zc forces zc < nbz) give
+    bitwise the same result as one chunk, element-wise within 1e-5 of FP64."""
+    rng = np.random.default_rng(43)
+    nb, M, K, N = 3, 2048, 4096, 128
+    A = _rand32(rng, (nb, 2, M, K))
+    B = _rand32(rng, (nb, 2, K, N))
+    B[2] *= np.float32(1e-4)
+    LIB.tn_debug_set_zc(zc)
+    try:
+        out = _contract_only(A, "sMk", B, "skN", "sMN", (nb, 2, M, N), nb, True, True, gemm=2)
+        LIB.tn_debug_set_zc(0)
+        ref0 = _contract_only(A, "sMk", B, "skN", "sMN", (nb, 2, M, N), nb, True, True, gemm=2)
+    finally:
+        LIB.tn_debug_set_zc(0)
+    assert np.array_equal(out, ref0)
+    ref = np.matmul(A.astype(np.complex128), B.astype(np.complex128))
+    err = np.abs(out - ref).max(axis=-1) / np.abs(ref).max(axis=-1)
+    print("per-sample-B max elementwise rel err", zc, err.max()); assert err.max() <= 1e-5, err.max()

@@ -227,6 +227,20 @@ def chain(n: int) -> Lattice:
     return lat
 
 
+def row_strip(lat: Lattice, b0: int, b1: int) -> Lattice:
+    """Rows b0..b1-1 of a lattice as a lattice of its own (vertices renumbered in row order,
+    edges among them kept, edge order preserved): a few rows of the full chip at the full
+    row widths, for exact-regime tests at the metric tensor shapes."""
+    keep = [v for r in lat.rows[b0:b1] for v in r]
+    new = {v: i for i, v in enumerate(keep)}
+    edges = [(new[u], new[v]) for (u, v) in lat.edges if u in new and v in new]
+    edges = [(min(e), max(e)) for e in edges]
+    rows = [[new[v] for v in r] for r in lat.rows[b0:b1]]
+    out = Lattice(f"{lat.name}_rows{b0}to{b1}", len(keep), edges, [lat.coords[v] for v in keep], rows)
+    out.colours = _bipartite_colouring(out.n, edges)
+    return out
+
+
 def by_name(name: str) -> Lattice:
     if name.startswith("square"):
         r, c = name[len("square"):].split("x")
