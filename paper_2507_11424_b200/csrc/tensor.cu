@@ -571,8 +571,6 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
   for (char ch : Ms) Msz *= dim[ch];
   for (char ch : Ns) Nsz *= dim[ch];
   for (char ch : Ks) Ksz *= dim[ch];
-  int nbx = X.bstride ? c.nb : 1;
-  int nby = Y.bstride ? c.nb : 1;
   bool per_out = X.bstride || Y.bstride;
 
   // choose the K order: keep whichever operand's order avoids a permute, else the larger's
@@ -584,7 +582,8 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
     return group_stride(oy, Ls) >= 0 && group_stride(oy, Ns) >= 0 && group_stride(oy, K) >= 0;
   };
   std::string Kord;
-  int64_t szx = X.size() * nbx, szy = Y.size() * nby;
+  // per-sample sizes: the K order (hence the summation order) must not depend on the batch
+  int64_t szx = X.size(), szy = Y.size();
   if (x_ok(Kx) && y_ok(Kx)) Kord = Kx;
   else if (x_ok(Ky) && y_ok(Ky)) Kord = Ky;
   else if (x_ok(Kx)) Kord = Kx;   // permute Y
