@@ -93,9 +93,14 @@ def test_amplitude_vs_oracle():
     la, ph = g.amplitude(x, 8)
     M, logs = B.norm_envs(P, 16)
     half_lnZ = 0.5 * B.log_norm(P, M, logs)
+    sector = sum(L.domain_wall_bits(lat))
+    n_rel = 0
     for k in range(len(x)):
         lr, pr = B.amplitude(P, x[k], 8)
-        assert amp_close(la[k], ph[k], lr, pr, half_lnZ), (k, la[k], lr, ph[k], pr)
+        forbidden = int(x[k].sum()) != sector  # U(1): <x|psi> = 0 exactly
+        n_rel += not forbidden
+        assert amp_close(la[k], ph[k], lr, pr, forbidden, half_lnZ), (k, la[k], lr, ph[k], pr)
+    assert n_rel >= 8
 
 
 @pytest.mark.parametrize("lat_name,chi,K,R", [("willow105", 4, 2, 8), ("square4x4", 4, 3, 16)])

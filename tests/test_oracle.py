@@ -79,18 +79,79 @@ def test_hash_init_vectorised_matches_scalar():
 
 
 def test_eq1_worked_example():
+    """Eq. (1) through the generator's own truncation (generator.apply2):
+    on a 4-qubit chain, Bell pairs on (0,1) and (2,3) and the operator
+    G = sum_k sqrt(w_k) P_k (x) P_k (P = I, X, Y, Z / sqrt 2) on the middle edge make the
+    (01|23) Schmidt spectrum equal the worked example's {0.8, 0.15, 0.04, 0.01} (the Choi state
+    of G); truncating the middle bond to chi = 2 must record eps = 0.05."""
     line = [l for l in open(os.path.join(GOLDEN, "eq1_discarded_weight.txt")) if not l.startswith("#")][0]
     spec, keep, want = line.split(";")
     w = np.array([float(x) for x in spec.split()])
-    sig = np.sqrt(w)
-    # build a 4x4 matrix with that spectrum and run the generator's SVD truncation rule
-    rng = np.random.default_rng(0)
-    U, _ = np.linalg.qr(rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4)))
-    V, _ = np.linalg.qr(rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4)))
-    m = U @ np.diag(sig) @ V.conj().T
-    s = np.linalg.svd(m, compute_uv=False)
-    eps = (s[int(keep):] ** 2).sum() / (s ** 2).sum()
-    assert abs(eps - float(want)) < 1e-12
+    I2 = np.eye(2)
+    X = np.array([[0, 1], [1, 0]], dtype=complex)
+    Y = np.array([[0, -1j], [1j, 0]])
+    Z = np.diag([1.0, -1.0]).astype(complex)
+    Gop = sum(np.sqrt(wk) * np.kron(Pk, Pk) / 2 for wk, Pk in zip(w, (I2, X, Y, Z)))
+    H = np.array([[1, 1], [1, -1]]) / np.sqrt(2)
+    CNOT = np.array([[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0]], dtype=complex)
+    bell = CNOT @ np.kron(H, I2)  # |00> -> (|00> + |11>)/sqrt 2, index 2 x_u + x_v
+    lat = L.chain(4)
+    tns = G.TNS(lat, [0, 0, 0, 0])
+    tns.bp()
+    tns.apply2(0, bell, 4)
+    tns.apply2(2, bell, 4)
+    assert tns.eps[-2:] == [0.0, 0.0]
+    tns.bp()
+    tns.apply2(1, Gop, int(keep))
+    assert abs(tns.eps[-1] - float(want)) < 1e-12, tns.eps[-1]
+
+
+def test_norm_estimate_pins():
+    """E_q[p/q] = <psi|psi> by oracle.metrics.norm_estimate.
+    (a) Worked example (tests/golden/norm_estimate_worked.txt): ratios {1, 2, 3, 4} ->
+    mean 2.5, standard error sqrt(5/3)/2. (b) Exact regime (config-1-like 3x3
+    state scaled so <psi|psi> != 1): q = p/<psi|psi> for every sample, so the estimate is
+    <psi|psi> of the brute-force statevector with zero spread."""
+    from oracle import metrics
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "norm_estimate_worked.txt"))
+            if l.strip() and not l.startswith("#")]
+    ratios = [float(x) for x in rows[0]]
+    want_mean, want_se = float(rows[1][0]), float(rows[1][1])
+    m, se = metrics.norm_estimate(np.zeros(len(ratios)), np.log(ratios))
+    assert abs(m - want_mean) < 1e-15 and abs(se - want_se) < 1e-12
+    lat = L.square(3, 3)
+    st = S.vidal_like(lat, 2, seed=3, xi=2.0)
+    st["tensors"] = [t * 1.3 for t in st["tensors"]]
+    psi = SV.statevector(st)
+    Z = np.vdot(psi, psi).real
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, 16)
+    u = S.uniforms(12, lat.n, 5)
+    logq, logp = [], []
+    for k in range(len(u)):
+        bits, lq, _, _ = B.sample(P, M, 16, u[k])
+        logq.append(lq)
+        logp.append(math.log(abs(psi[int("".join(map(str, bits)), 2)]) ** 2))
+    m, se = metrics.norm_estimate(logq, logp)
+    assert abs(m / Z - 1) < 1e-10 and se < 1e-10 * Z
+
+
+def test_importance_expectation_product_state():
+    """PAPER.md:297-300, observable Z_i (not the identity): samples = all 2^N basis states with
+    uniform q, p = |<x|psi>|^2 of a product state prod_v (a_v|0> + b_v|1>); the importance
+    estimate of <Z_i> must equal the closed form (|a_i|^2 - |b_i|^2) / (|a_i|^2 + |b_i|^2)."""
+    from oracle import metrics
+    rng = np.random.default_rng(4)
+    n = 5
+    ab = rng.standard_normal((n, 2)) + 1j * rng.standard_normal((n, 2))
+    xs = np.array(list(itertools.product([0, 1], repeat=n)))
+    amp = np.array([np.prod([ab[v, x[v]] for v in range(n)]) for x in xs])
+    logp = np.log(np.abs(amp) ** 2)
+    logq = np.full(len(xs), -n * math.log(2))
+    for i in range(n):
+        zi = 1 - 2 * xs[:, i]
+        want = (abs(ab[i, 0]) ** 2 - abs(ab[i, 1]) ** 2) / (abs(ab[i, 0]) ** 2 + abs(ab[i, 1]) ** 2)
+        assert abs(metrics.importance_expectation(logq, logp, zi) - want) < 1e-12
 
 
 def test_heisenberg_gate_closed_form():
