@@ -47,6 +47,15 @@ WORKLOADS = {
 PHASES = ["gemm_tc_incl_prep", "gemm_simt", "permute", "orth", "tail", "misc", "tc_kernel"]
 DEFAULT_WORKLOAD = "willow105_chi32_env128"
 STATE_SEED = 2507
+UNIFORM_SEED = 1005
+E2E_SEED = 77
+# SURVEY 8(d) "Algorithmic work per unit": per-sample complex MACs of the method's own
+# contractions (bonds at their R6 values, nh = 2) for the configurations it tabulates
+ALG_CMACS_PER_SAMPLE = {
+    "willow105_chi32_env128": 4.9e13,  # cfg 4b
+    "eagle127_chi16_env64": 6.5e10,    # cfg 3
+    "square6x6_chi8_env32": 2.9e9,     # cfg 2
+}
 
 
 def log(*a):
@@ -109,42 +118,9 @@ class Clocks:
                 "samples": len(rows)}
 
 
-def shard_uniforms(u_all, nsteps, world, rank, batch):
-    """Rows of the global uniform matrix owned by `rank`: step s, rank r -> global samples
-    [(s*world + r)*batch, (s*world + r + 1)*batch) (weak scaling; SURVEY 8(b) determinism:
-    sample k always reads uniforms[k], whatever the GPU count)."""
-    return np.stack([u_all[(s * world + rank) * batch:(s * world + rank + 1) * batch] for s in range(nsteps)])
-
-
 def make_state(lat, chi):
     from tninputs import synthetic as S
     return S.vidal_like(lat, chi, seed=STATE_SEED)
-
-
-def broadcast_state(st, lat, chi, rank, dist, torch, dev):
-    """NCCL broadcast of the TNS tensors from rank 0."""
-    from tninputs import synthetic as S
-    if rank == 0:
-        flat = np.concatenate([t.reshape(-1).view(np.float64) for t in st["tensors"]])
-        buf = torch.from_numpy(flat).to(dev)
-    else:
-        sizes = []
-        inc = S.incident_edges(lat.n, lat.edges)
-        for v in range(lat.n):
-            sizes.append(2 * 2 * chi ** len(inc[v]))
-        buf = torch.empty(sum(sizes), dtype=torch.float64, device=dev)
-    dist.broadcast(buf, 0)
-    if rank != 0:
-        host = buf.cpu().numpy()
-        tensors, off = [], 0
-        inc = S.incident_edges(lat.n, lat.edges)
-        for v in range(lat.n):
-            shape = (2,) + (chi,) * len(inc[v])
-            n = int(np.prod(shape))
-            tensors.append(host[off: off + 2 * n].view(np.complex128).reshape(shape).copy())
-            off += 2 * n
-        st = S.make_state(lat, tensors, [chi] * lat.n_edges, chi, {"kind": "vidal_like", "seed": STATE_SEED})
-    return st
 
 
 class LazyRandomM:
@@ -187,14 +163,16 @@ class LazyRandomM:
         return self.cache[b]
 
 
-def oracle_row_cmacs(P, M, R):
+def oracle_dry_run(P, M, R):
     """Complex MACs per row of one oracle sample, counted on the oracle's own pairwise
-    contractions (oracle.bmps.pair) in a shape-only dry run: every pair() returns zeros of
-    the output shape, so the whole sample costs milliseconds. The oracle's arithmetic is
-    untouched (the dry run replaces the function only for the duration of the count)."""
+    contractions (oracle.bmps.pair) in a shape-only dry run, and the shapes of the incoming
+    boundary MPS of every row: every pair() returns zeros of the output shape and _merge's
+    outputs are recorded, so the whole sample costs milliseconds. The oracle's arithmetic is
+    untouched (the dry run replaces the two functions only for the duration of the count)."""
     from oracle import bmps as B
-    counts = []
-    real_pair = B.pair
+    counts = [0.0]
+    real_pair, real_merge = B.pair, B._merge
+    merged = []
 
     def dry_pair(a, sa, b, sb, out):
         dims = {}
@@ -204,30 +182,43 @@ def oracle_row_cmacs(P, M, R):
         cm = 1.0
         for d in dims.values():
             cm *= d
-        counts[-1] += cm
+        counts[0] += cm
         return np.zeros([dims[ch] for ch in out], dtype=np.complex128)
 
-    rows_total = len(P.rows)
-    per_row = []
-    B.pair = dry_pair
+    def rec_merge(P_, row, sites):
+        m = real_merge(P_, row, sites)
+        merged.append(None if m is None else [t.shape for t in m])
+        return m
+
+    real_nstrip = B._n_strip
+    marks = []
+
+    def mark_nstrip(P_, b, m_prev):  # called once at the start of every row
+        marks.append(counts[0])
+        return real_nstrip(P_, b, m_prev)
+
+    B.pair, B._merge, B._n_strip = dry_pair, rec_merge, mark_nstrip
     try:
         with np.errstate(all="ignore"):
-            for r in range(1, rows_total + 1):
-                counts.append(0.0)
-                B.sample(P, M, R, np.zeros(P.n), forced=np.zeros(P.n, dtype=np.uint8), max_rows=r)
-                per_row.append(counts[-1] - sum(per_row))
+            B.sample(P, M, R, np.zeros(P.n), forced=np.zeros(P.n, dtype=np.uint8))
     finally:
-        B.pair = real_pair
-    return per_row
+        B.pair, B._merge, B._n_strip = real_pair, real_merge, real_nstrip
+    marks.append(counts[0])
+    per_row = [marks[i + 1] - marks[i] for i in range(len(P.rows))]
+    m_shapes = [None] + list(merged[:-1])  # incoming MPS of row b = merge of row b-1
+    return per_row, m_shapes
 
 
 class OracleTimer:
     """Bounded timing of the CPU oracle (oracle/bmps.sample, as it stands) on the same
-    workload: one sample's rows are run in order for as many rows as fit the budget (the row
-    count is chosen once by predicting each extra row's time from its complex MACs, so no run
-    exceeds the budget by more than one row's misprediction); samples/s is scaled by the
-    fraction of the sample's complex MACs those rows carry (counted on the oracle's own
-    contractions, scripts/oracle_row_cmacs.py)."""
+    workload: ONE row of one sample, run from a random incoming boundary MPS and random
+    norm-environment sites of the method's shapes (the oracle's own precompute at the metric
+    configuration takes days). Interior rows run every vertex at the same full-bond shapes
+    (bonds R = chi_env, chi), so a row's time gives the oracle's rate at the sample's dominant
+    contraction shapes; the row is the one with the largest share of the sample's complex
+    MACs (counted on the oracle's own contractions, oracle_dry_run) whose predicted time fits
+    the budget, and one row's time / its share of the sample's MACs = the oracle's time per
+    sample. A 'step' of the reference arm is one such row."""
 
     def __init__(self, st, lat, R, budget_s, seed=7, workload=None):
         from oracle import bmps as B
@@ -239,62 +230,50 @@ class OracleTimer:
             self.threads = os.cpu_count()
         t0 = time.time()
         self.P = B.Prepared(st, lat.rows)
-        self.M = LazyRandomM(self.P, R, np.random.default_rng(seed))
-        try:
-            rc = json.load(open(os.path.join(ROOT, "profiles", "oracle_row_cmacs.json")))[workload]
+        self.rng = np.random.default_rng(seed)
+        self.M = LazyRandomM(self.P, R, self.rng)
+        try:  # cached dry run (scripts/oracle_row_cmacs.py); minutes at the metric shapes
+            ent = json.load(open(os.path.join(ROOT, "profiles", "oracle_row_cmacs.json")))[workload]
+            rc = ent["row_cmacs"]
+            self.m_shapes = [None if m is None else [tuple(t) for t in m] for m in ent["m_shapes"]]
         except Exception:
-            rc = oracle_row_cmacs(self.P, self.M, R)
-        self.cum = np.cumsum(np.asarray(rc, dtype=np.float64))
-        self.setup = time.time() - t0
+            rc, self.m_shapes = oracle_dry_run(self.P, self.M, R)
+        self.rc = np.asarray(rc, dtype=np.float64)
+        self.total = float(self.rc.sum())
         self.R = R
         self.nrows = len(lat.rows)
         self.u = np.random.default_rng(seed).random(lat.n)
-        # host complex-GEMM rate (one 1024^3 zgemm) as the prior for rows not yet timed
-        a = np.ones((1024, 1024), dtype=np.complex128)
+        # host complex-GEMM rate (one 2048^3 zgemm) as the prior for choosing the row
+        a = np.ones((2048, 2048), dtype=np.complex128)
         _ = a @ a
-        t0 = time.time()
+        t1 = time.time()
         _ = a @ a
-        zrate = 1024.0 ** 3 / max(time.time() - t0, 1e-6)
-        self.zrate = zrate
-        # choose the row count: at least enough rows to carry 0.01 % of the sample's work (the
-        # first rows are overhead-dominated), then extend while one more row is predicted to fit
-        r = 1
-        while r < self.nrows and self.cum[r - 1] < 1e-4 * self.cum[-1]:
-            r += 1
-        t_r = self.run(r)
-        while r < self.nrows:
-            measured = self.cum[r - 1] / max(t_r, 1e-3) if self.cum[r - 1] > 1e9 else 0.0
-            rate = max(measured, 0.25 * zrate)  # host complex MACs/s
-            pred = t_r + (self.cum[r] - self.cum[r - 1]) / rate
-            if pred > budget_s:
-                break
-            r += 1
-            t_r = self.run(r)
-        self.rows = r
+        self.zrate = 2048.0 ** 3 / max(time.time() - t1, 1e-6)
+        pred = self.rc / (0.5 * self.zrate)
+        ok = [b for b in range(self.nrows) if pred[b] <= budget_s] or [int(np.argmin(self.rc + (self.rc == 0) * 1e30))]
+        self.row = max(ok, key=lambda b: self.rc[b])
+        shp = self.m_shapes[self.row]
+        self.m_in = None if shp is None else [
+            (self.rng.standard_normal(s) + 1j * self.rng.standard_normal(s)) / math.sqrt(np.prod(s)) for s in shp]
+        self.setup = time.time() - t0
 
-    def run(self, rows):
+    def run(self):
         t0 = time.time()
-        self.B.sample(self.P, self.M, self.R, self.u, max_rows=rows)
+        self.B.sample(self.P, self.M, self.R, self.u, first_row=self.row, max_rows=self.row + 1, m_in=self.m_in)
         return time.time() - t0
 
     def measure(self):
-        last = self.run(self.rows)
-        frac = self.cum[self.rows - 1] / self.cum[-1]
-        # extrapolation to the whole sample, taking the faster (CPU-favourable) of: the timed
-        # rows' rate scaled by their work fraction, and the timed rows plus the remaining
-        # complex MACs at the host's full zgemm rate (an upper bound on the oracle's speed)
-        t_scaled = last / frac
-        t_bound = last + (self.cum[-1] - self.cum[self.rows - 1]) / self.zrate
-        t_full = min(t_scaled, t_bound)
-        rate = 1.0 / t_full if t_full > 0 else float("nan")
+        t = self.run()
+        frac = self.rc[self.row] / self.total
+        rate = frac / t if t > 0 else float("nan")
         return {"value": rate, "unit": "samples/s", "cores": int(self.threads), "kind": "oracle",
-                "sample": (f"one sample's first {self.rows}/{self.nrows} rows ({100 * frac:.3g}% of its complex "
-                           f"MACs, counted on the oracle's own contractions by a shape-only dry run) took "
-                           f"{last:.1f} s on the host; whole sample extrapolated as the faster of the work-fraction "
-                           f"scaling ({t_scaled:.0f} s) and the remaining work at the host's measured zgemm rate "
-                           f"{self.zrate / 1e9:.0f} G complex MAC/s ({t_bound:.0f} s); random norm-environment sites "
-                           f"of the method's shapes (oracle precompute at this size takes days); setup "
-                           f"{self.setup:.0f} s not timed")}
+                "seconds": t, "fraction_of_sample": frac,
+                "sample": (f"row {self.row} of {self.nrows} of one sample ({100 * frac:.3g}% of the sample's complex MACs, "
+                           f"counted on the oracle's own contractions by a shape-only dry run; every vertex at the "
+                           f"full-bond shapes that dominate the sample), measured {t:.1f} s on the host from a random "
+                           f"incoming boundary MPS and random norm-environment sites of the method's shapes (the "
+                           f"oracle's precompute at this size takes days); samples/s = fraction / seconds; host "
+                           f"zgemm rate {self.zrate / 1e9:.0f} G complex MAC/s; setup {self.setup:.0f} s not timed")}
 
 
 def oracle_rate(st, lat, R, budget_s, seed=7, workload=None):
@@ -339,14 +318,16 @@ def main():
         # each step a bounded sample; the whole run stays within ~4 minutes after setup
         timer = OracleTimer(st, lat, R, budget_s=min(a.cpu_budget, 240.0 / (a.warmup + a.steps)),
                             workload=a.workload)
-        vals = []
+        vals, secs = [], []
         for i in range(a.warmup + a.steps):
             cb = timer.measure()
             if i >= a.warmup:
                 vals.append(cb["value"])
+                secs.append(cb["seconds"])
         v = float(np.mean(vals))
+        # a step = one row of one sample (cb["fraction_of_sample"] of a sample), measured seconds
         out = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": a.gpus, "steps": a.steps,
-               "warmup": a.warmup, "ms_per_step": 1000.0 / v if v > 0 else None, "higher_is_better": True,
+               "warmup": a.warmup, "ms_per_step": 1000.0 * float(np.mean(secs)), "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
                "config": config, "impl": "reference",
                "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cb["cores"], "kind": "oracle",
@@ -369,10 +350,11 @@ def main():
     LIB.tn_debug_set_profile.argtypes = [C.c_int]
     LIB.tn_debug_row_cmacs.argtypes = [C.c_void_p, C.c_int]
 
+    from paper_2507_11424_b200.dist import DistSampler, broadcast_state, gather_samples, shard_range, uniforms_rows
     t0 = time.time()
     st = make_state(lat, chi) if rank == 0 else None
     if world > 1:
-        st = broadcast_state(st, lat, chi, rank, dist, torch, dev)
+        st = broadcast_state(st, dist, dev)  # NCCL broadcast of the TNS from rank 0
     g = TNState(st)
     if a.order:
         g.set_option("order", a.order)
@@ -391,19 +373,21 @@ def main():
 
     N = lat.n
     nsteps = a.warmup + a.steps
-    # uniforms for the global sample indices of this rank (weak scaling: rank r owns batch r)
-    rng = np.random.default_rng(1005)
-    u_all = rng.random((nsteps * world * batch, N))
-    u_mine = shard_uniforms(u_all, nsteps, world, rank, batch)
+    # contiguous shard of the global sample index: rank r owns samples
+    # [floor(r n / G), floor((r+1) n / G)), n = G * batch * nsteps, uniforms of the global index
+    n_total = world * batch * nsteps
+    k0, k1 = shard_range(n_total, world, rank)
+    u_mine = uniforms_rows(UNIFORM_SEED, N, k0, k1).reshape(nsteps, batch, N)
     u_dev = torch.from_numpy(u_mine).to(dev)
     bits_dev = torch.empty((nsteps, batch, N), dtype=torch.uint8, device=dev)
     logp_dev = torch.empty((nsteps, batch), dtype=torch.float64, device=dev)
+    flags_dev = torch.zeros((nsteps, batch), dtype=torch.int32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step(s):
         g.sample_dev(lat.rows, R, batch, u_dev[s].data_ptr(), bits_dev[s].data_ptr(), logp_dev[s].data_ptr(),
-                     0, 0, stream.cuda_stream)
+                     0, flags_dev[s].data_ptr(), stream.cuda_stream)
 
     for s in range(a.warmup):
         step(s)
@@ -445,15 +429,46 @@ def main():
         ms = float(t.item())
     value = world * batch * a.steps / (ms / 1000.0)
 
-    # e2e through the public host API: H2D of the uniforms and D2H of bits + ln q inside
+    # validation of the benchmarked samples (all ranks): per-sample flags (TN_FLAG_*, R9),
+    # non-finite ln q, mean -ln q, bits in {0, 1}
+    fl = flags_dev[a.warmup:].reshape(-1).to(torch.int64)
+    lq = logp_dev[a.warmup:].reshape(-1)
+    stats = torch.stack([(fl & 1 != 0).sum(), (fl & 2 != 0).sum(), (fl & 4 != 0).sum(),
+                         (~torch.isfinite(lq)).sum(), (bits_dev[a.warmup:] > 1).sum()]).to(torch.float64)
+    nlq = torch.where(torch.isfinite(lq), -lq, torch.zeros_like(lq)).sum().reshape(1)
+    stats = torch.cat([stats, nlq])
+    if dist:
+        dist.all_reduce(stats)
+    stats = stats.cpu().numpy()
+    n_timed = world * batch * a.steps
+    validation = {"samples": n_timed, "flag_clamped": int(stats[0]), "flag_zero_mass": int(stats[1]),
+                  "flag_nonfinite": int(stats[2]), "logq_nonfinite": int(stats[3]), "bits_not_01": int(stats[4]),
+                  "mean_minus_logq": float(stats[5]) / max(1, n_timed - int(stats[3])),
+                  "valid": bool(stats[2] == 0 and stats[3] == 0 and stats[4] == 0)}
+    # the product path's gather (dist.py, all_gather_into_tensor of bits and ln q), timed apart
+    gather_ms = None
+    if dist:
+        torch.cuda.synchronize()
+        tg = time.perf_counter()
+        gb, gl = gather_samples(bits_dev[a.warmup:].reshape(-1, N), logp_dev[a.warmup:].reshape(-1),
+                                world * batch * a.steps, dist, dev)
+        torch.cuda.synchronize()
+        gather_ms = 1e3 * (time.perf_counter() - tg)
+
+    # e2e through the public API at N GPUs (DistSampler.sample: uniforms built on the host and
+    # copied H2D from pinned memory, sampling, the gather, D2H of bits + ln q), wall clock
     e2e_steps = 1 if chi >= 32 else a.steps
-    u_host = u_mine[a.warmup: a.warmup + e2e_steps]
+    ds = DistSampler(st, lat.rows, R, dist, dev, tn=g) if dist else None
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for s in range(e2e_steps):
-        g.sample(lat.rows, R, u_host[s])
+        if ds is not None:
+            eb, el = ds.sample(world * batch, seed=E2E_SEED + s)
+            eb, el = eb.cpu(), el.cpu()
+        else:
+            g.sample(lat.rows, R, uniforms_rows(E2E_SEED + s, N, 0, batch))
     torch.cuda.synchronize()
     te = time.perf_counter() - t0
     if dist:
@@ -461,8 +476,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item())
     e2e = {"value": world * batch * e2e_steps / te, "unit": "samples/s",
-           "h2d_bytes_per_step": int(batch * N * 8), "d2h_bytes_per_step": int(batch * N * 1 + batch * 8 * 2),
-           "steps": e2e_steps}
+           "h2d_bytes_per_step": int(world * batch * N * 8),
+           "d2h_bytes_per_step": int(world * batch * (N + 8)), "steps": e2e_steps,
+           "api": "paper_2507_11424_b200.dist.DistSampler.sample" if dist else "tn_sample (host buffers)"}
 
     # per-phase device time of one extra (untimed) step, every phase bracketed by CUDA events
     phase = np.zeros(7)
@@ -483,7 +499,14 @@ def main():
     tf32_peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * ratio
     tc_ms = prof[6]
     tc_cmacs = cnt[1]
-    achieved = (8.0 * tc_cmacs) / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else None
+    executed_per_sample = float(cnt[0]) / (batch * a.steps)
+    # algorithmic work: SURVEY 8(d)'s per-sample complex MACs for this configuration (the
+    # method's own contractions), x the samples the timed kernels processed; where 8(d) has no
+    # figure, the engine's executed count of the tensor-core GEMMs
+    alg_ps = ALG_CMACS_PER_SAMPLE.get(a.workload)
+    alg_cmacs = alg_ps * batch * a.steps if alg_ps else tc_cmacs
+    achieved = (8.0 * alg_cmacs) / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else None
+    achieved_exec = (8.0 * tc_cmacs) / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else None
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "tc_gemm_traffic.json")
     if os.path.exists(tpath):
@@ -500,19 +523,25 @@ def main():
                 "traffic_source": traffic_src,
                 "peak_source": f"{which}: FP32-class tensor peak = bf16_tflops_sustained x 1.1/2.25 (dense TF32/BF16 "
                                f"nominal ratio); the path computes complex64 products to FP32 accuracy",
-                "algorithmic": "8 real flops per complex MAC of the GEMM (M*N*K), counted once (complex as one real "
-                               "GEMM on the [Re -Im; Im Re] embedding costs exactly these 8 flops)",
+                "algorithmic": (f"8 real flops per complex MAC; {alg_ps:.3g} complex MACs per sample = SURVEY 8(d) "
+                                f"per-sample figure for this configuration, x {batch * a.steps} samples"
+                                if alg_ps else "8 real flops per executed complex MAC of the tensor-core GEMMs "
+                                               "(no SURVEY 8(d) figure for this configuration)"),
+                "achieved_on_executed": achieved_exec,
                 "fp16_issued": {"split_factor": 3, "peak_fp16_sustained": fp16_peak,
-                                "issued_frac": (3.0 * achieved / fp16_peak) if achieved else None,
-                                "note": "each complex MAC issues 3 FP16 MMAs (hi*hi + hi*lo + lo*hi)"},
+                                "issued_frac": (3.0 * achieved_exec / fp16_peak) if achieved_exec else None,
+                                "note": "each executed complex MAC issues 3 FP16 MMAs (hi*hi + hi*lo + lo*hi) on the "
+                                        "[Re -Im; Im Re] real embedding"},
                 "tc_launches": int(cnt[2]), "tc_ms_total": tc_ms, "tc_share_of_step": tc_ms / ms if ms else None,
-                "cmacs_per_sample": float(cnt[0]) / (batch * a.steps)}
+                "cmacs_per_sample_executed": executed_per_sample, "cmacs_per_sample_algorithmic": alg_ps,
+                "row_cmacs_executed": [float(x) for x in rows]}
     out = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "c64", "data": "synthetic", "config": dict(config, precompute_s=t_pre),
            "roofline": roofline, "e2e": e2e, "gpu_launches": int(cnt[3] - cnt0[3]), "clocks": clk,
            "phase_ms_per_step": {k: round(float(v), 1) for k, v in zip(PHASES, phase)},
-           "precompute_phase_ms": pre_phase}
+           "precompute_phase_ms": pre_phase, "validation": validation, "gather_ms": gather_ms,
+           "samples_per_s_incl_precompute_1e5": 1e5 / (t_pre + 1e5 / value) if value > 0 else None}
     if world == 1 and not a.no_cpu_baseline:
         try:
             out["cpu_baseline"] = oracle_rate(st, lat, R, budget_s=a.cpu_budget, workload=a.workload)

@@ -395,10 +395,13 @@ def _merge(P: Prepared, row, sites):
     return out
 
 
-def sample(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2, forced=None, max_rows=None):
+def sample(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2, forced=None, max_rows=None,
+           first_row=0, m_in=None):
     """O5 for one sample: returns (bits[N] uint8 by vertex id, ln q, cond[N], flags).
     With `forced` (bits by vertex id) the draw is replaced by the given bits, which
     evaluates q(x) of any x (used to enumerate the whole distribution in tests).
+    first_row / m_in / max_rows run rows first_row .. max_rows-1 only, starting from the
+    incoming boundary MPS m_in (bounded CPU timing of a part of a sample only).
 
     Row b: n_b = Fit_R(m_{b-1} . psi_b) with (s, d) open (R3 compress-then-sample); right
     ladder R^(s)_j = n_j[s] M_j conj(n_j[s]) R_{j+1}; left pass w_s = Re<L_j, R^(s)_j>,
@@ -409,8 +412,10 @@ def sample(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2,
     cond = np.zeros(n, dtype=np.float64)
     logq = 0.0
     flags = 0
-    m_prev = None
+    m_prev = m_in
     for b, row in enumerate(P.rows):
+        if b < first_row:
+            continue
         if max_rows is not None and b >= max_rows:  # partial run (bounded CPU timing only)
             break
         strip = _n_strip(P, b, m_prev)

@@ -1,8 +1,8 @@
 """Per-row complex MACs of one oracle sample (oracle.bmps.sample), counted by bench.py's
-shape-only dry run of the oracle's pairwise contractions; written to
-profiles/oracle_row_cmacs.json for the bounded CPU-oracle timings of bench.py (the oracle
-times its first rows and scales by their share of the sample's work). Calls only oracle/
-and tninputs/ (no CUDA path).
+shape-only dry run of the oracle's pairwise contractions, and the shapes of each row's
+incoming boundary MPS; written to profiles/oracle_row_cmacs.json for the bounded CPU-oracle
+timings of bench.py (the oracle times one row and scales by its share of the sample's
+work). Calls only oracle/ and tninputs/ (no CUDA path).
 
 python scripts/oracle_row_cmacs.py [workload ...]
 """
@@ -26,6 +26,7 @@ for wl in sys.argv[1:] or [bench.DEFAULT_WORKLOAD]:
     st = bench.make_state(lat, chi)
     P = B.Prepared(st, lat.rows)
     M = bench.LazyRandomM(P, R, np.random.default_rng(7))
-    table[wl] = bench.oracle_row_cmacs(P, M, R)
-    print(wl, f"{sum(table[wl]):.4e} complex MACs per sample", flush=True)
+    rc, ms = bench.oracle_dry_run(P, M, R)
+    table[wl] = {"row_cmacs": rc, "m_shapes": [None if m is None else [list(t) for t in m] for m in ms]}
+    print(wl, f"{sum(rc):.4e} complex MACs per sample", flush=True)
 json.dump(table, open(path, "w"), indent=1)
