@@ -117,21 +117,6 @@ struct Ops {
     return contract(c, X2, "xbDfsur", false, A, "sUDbR", true, "xfurUR");
   }
 
-  // rmid2(F, j) for the output-bond rows [z0, z1) of F: [z, e, l, L, u, U], the right-hand
-  // mirror of mid2 (same cost).
-  Tensor rmid2(const Tensor& F, int j, int z0, int z1) {
-    const Tensor& A = s.mats[j];
-    Tensor Fc = slice_rows(F, z0, z1);
-    Tensor Z2a;
-    if (s.tops[j].p) {
-      Tensor Z1 = contract(c, Fc, "zfrR", false, s.tops[j], "edDf", false, "zrRedD");
-      Z2a = contract(c, Z1, "zrRedD", false, A, "sudlr", false, "zReDsul");
-    } else {
-      Z2a = contract(c, Fc, "zerR", false, A, "sudlr", false, "zResul");  // identity top: f = e, d = D = 1
-    }
-    return contract(c, Z2a, "zReDsul", false, A, "sUDLR", true, "zelLuU");
-  }
-
   int chunk_rows(int j, int nx) {
     const Tensor& A = s.mats[j];
     int64_t u = A.shape[1], d = A.shape[2], l = A.shape[3], r = A.shape[4];
@@ -172,11 +157,8 @@ struct Ops {
   }
 
   // d = d<o|T>/d conj(o_j) = L . (column j) . F, contracted from the left
-  // (mid1 / mid2). Double layer: when E is non-null it also accumulates, chunk by chunk of the
-  // mid contraction, E[z, f, r, R] = sum X . conj(d) -- the new left environment in the basis
-  // of d, so that after o = d W (left_orth) the environment is E conj(W) without a second
-  // evaluation of the mid contraction.
-  Tensor derivative(const Tensor& L, int j, const Tensor& F, Tensor* E = nullptr) {
+  // (mid1 / mid2).
+  Tensor derivative(const Tensor& L, int j, const Tensor& F) {
     if (!s.dbl) {
       Tensor X = mid1(L, j);
       return contract(c, X, "xnpr", false, F, "znr", false, "xpz");
@@ -188,11 +170,6 @@ struct Ops {
       int x1 = std::min(nx, x0 + step);
       Tensor X = mid2(L, j, x0, x1);
       Tensor part = contract(c, X, "xfurUR", false, F, "zfrR", false, "xuUz");
-      if (E) {
-        Tensor e = contract(c, X, "xfurUR", false, part, "xuUz", true, "zfrR");
-        if (!E->p) *E = e;
-        else add_into(c, *E, e, 1);
-      }
       if (step >= nx) return part;
       if (!out.p) out = new_tensor(c, {nx, part.shape[1], part.shape[2], part.shape[3]}, false);
       copy_rows(c, part, out, x0, 1);
@@ -200,40 +177,11 @@ struct Ops {
     return out;
   }
 
-  // The same derivative contracted from the right (rmid1 / rmid2), for right-to-left
-  // half-sweeps. Double layer: E (if non-null) accumulates E[x, e, l, L] = sum Z . conj(d),
-  // the new right environment in the basis of d (o = W^H d after right_orth gives W^T E).
-  Tensor derivative_right(const Tensor& L, int j, const Tensor& F, Tensor* E = nullptr) {
-    if (!s.dbl) {
-      Tensor Z = rmid1(F, j);
-      return contract(c, L, "xmy", false, Z, "zmpy", false, "xpz");
-    }
-    const Tensor& A = s.mats[j];
-    int nz = F.shape[0];
-    int64_t u = A.shape[1], dd = A.shape[2], l = A.shape[3];
-    int64_t r = F.shape[2], R = F.shape[3];
-    int64_t e = s.tops[j].p ? s.tops[j].shape[0] : s.topbond[j];
-    // elements per z row of Z1 [z,r,R,e,d,D], Z2a [z,R,e,D,s,u,l], Z2 [z,e,l,L,u,U]
-    int64_t per = std::max({r * R * e * dd * dd, 2 * R * e * dd * u * l, e * l * l * u * u});
-    int step = (int)std::max<int64_t>(1, std::min<int64_t>(nz, s.chunk_elems / std::max<int64_t>(1, per)));
-    Tensor dT;  // [z, x, u, U]
-    for (int z0 = 0; z0 < nz; z0 += step) {
-      int z1 = std::min(nz, z0 + step);
-      Tensor Z = rmid2(F, j, z0, z1);
-      Tensor part = contract(c, L, "xelL", false, Z, "zelLuU", false, "zxuU");
-      if (E) {
-        Tensor ee = contract(c, Z, "zelLuU", false, part, "zxuU", true, "xelL");
-        if (!E->p) *E = ee;
-        else add_into(c, *E, ee, 1);
-      }
-      if (step >= nz) {
-        dT = part;
-        break;
-      }
-      if (!dT.p) dT = new_tensor(c, {nz, part.shape[1], part.shape[2], part.shape[3]}, false);
-      copy_rows(c, part, dT, z0, 1);
-    }
-    return permute(c, dT, "zxuU", "xuUz");
+  // The single-layer derivative contracted from the right (rmid1), for right-to-left
+  // half-sweeps: the same Z then gives the new right environment (absorb_right).
+  Tensor derivative_right(const Tensor& L, int j, const Tensor& F) {
+    Tensor Z = rmid1(F, j);
+    return contract(c, L, "xmy", false, Z, "zmpy", false, "xpz");
   }
 
   Tensor absorb_right(const Tensor& F, int j, const Tensor* o) {
@@ -299,25 +247,8 @@ void nan_check(Ctx& c, const char* what, const Tensor& t, int nb) {
 }
 
 namespace {
-// Map of an orthonormalisation (OrthTransform): W [D][D] (shared fit only, nb = 1) and
-// whether it is valid (full rank; read back to the host).
-struct Map {
-  Tensor W;
-  bool valid = false;
-};
-
-Map take_map(Ctx& c, Tensor& W, DevBuf& full) {
-  int h = 0;
-  TN_CUDA(cudaMemcpyAsync(&h, full.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  TN_CUDA(cudaStreamSynchronize(c.stream));
-  Map m;
-  m.W = W;
-  m.valid = h != 0;
-  return m;
-}
-
 // column span of o reshaped (prod(shape[:-1])) x shape[-1]
-Tensor left_orth(Ctx& c, const Tensor& o, int nb, Map* map = nullptr) {
+Tensor left_orth(Ctx& c, const Tensor& o, int nb) {
   Tensor q = new_tensor_n(c, o.shape, nb);
   if (!o.bstride) q.bstride = 0;
   int n = o.shape.back();
@@ -325,22 +256,13 @@ Tensor left_orth(Ctx& c, const Tensor& o, int nb, Map* map = nullptr) {
   MatView X{o.p, o.bstride, n, 1, false, m, n};
   MatView Q{q.p, q.bstride, n, 1, false, m, n};
   nan_check(c, "left_orth in", o, nb);
-  if (map && !o.bstride) {
-    Tensor W = new_tensor_n(c, {n, n}, 1);
-    W.bstride = 0;
-    DevBuf full(sizeof(int), c.stream);
-    OrthTransform tr{W.p, full.as<int>()};
-    orthonormalize(c, X, Q, nullptr, 1, &tr);
-    *map = take_map(c, W, full);
-  } else {
-    orthonormalize(c, X, Q, nullptr, o.bstride ? nb : 1);
-  }
+  orthonormalize(c, X, Q, nullptr, o.bstride ? nb : 1);
   nan_check(c, "left_orth out", q, nb);
   return q;
 }
 
 // row span of o reshaped shape[0] x (rest); optional C with o = C^H-factor (see linalg.h)
-Tensor right_orth(Ctx& c, const Tensor& o, int nb, Tensor* Cout, Map* map = nullptr) {
+Tensor right_orth(Ctx& c, const Tensor& o, int nb, Tensor* Cout) {
   Tensor q = new_tensor_n(c, o.shape, nb);
   if (!o.bstride) q.bstride = 0;
   int dl = o.shape[0];
@@ -354,16 +276,7 @@ Tensor right_orth(Ctx& c, const Tensor& o, int nb, Tensor* Cout, Map* map = null
     cp = Cout->p;
   }
   nan_check(c, "right_orth in", o, nb);
-  if (map && !o.bstride) {
-    Tensor W = new_tensor_n(c, {dl, dl}, 1);
-    W.bstride = 0;
-    DevBuf full(sizeof(int), c.stream);
-    OrthTransform tr{W.p, full.as<int>()};
-    orthonormalize(c, X, Q, cp, 1, &tr);
-    *map = take_map(c, W, full);
-  } else {
-    orthonormalize(c, X, Q, cp, o.bstride ? nb : 1);
-  }
+  orthonormalize(c, X, Q, cp, o.bstride ? nb : 1);
   nan_check(c, "right_orth out", q, nb);
   if (Cout) nan_check(c, "right_orth C", *Cout, nb);
   return q;
@@ -493,33 +406,16 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
   for (int k = K - 1; k >= 1; --k) Fk[k - 1] = env_right(Fk[k], k);
   // environments the current centre was computed with (for its true scale)
   Env cl = Lk[0], cf = Fk[0];
-  // Double layer (shared, nb = 1): the derivative's chunk loop also accumulates E = sum
-  // X . conj(d) (or Z . conj(d) from the right); where the orthonormalisation's map W is
-  // valid (o = d W, full rank) the new environment is E conj(W) (or W^T E), so the mid
-  // contraction runs once per site and half-sweep. TN_FIT_REUSE=0 disables it (A/B only).
-  static const bool reuse_env = !(getenv("TN_FIT_REUSE") && std::atoi(getenv("TN_FIT_REUSE")) == 0);
-  const bool dbl_reuse = s.dbl && !s.per_sample && reuse_env;
-  auto env_left_from = [&](const Env& Lk_, int k, const Tensor& E, const Map& mp) {
-    Env L = rescaled(contract(c, E, "zfrR", false, mp.W, "zy", true, "yfrR"), Lk_);
-    int end = (k + 1 < K) ? cols[k + 1] : s.W;
-    for (int j = cols[k] + 1; j < end; ++j) L = rescaled(ops.absorb_left(L.t, j, nullptr), L);
-    return L;
-  };
-  auto env_right_from = [&](const Env& Fk_, int k, const Tensor& E, const Map& mp) {
-    Env F = rescaled(contract(c, mp.W, "xy", false, E, "xelL", false, "yelL"), Fk_);
-    int start = (k >= 1) ? cols[k - 1] : -1;
-    for (int j = cols[k] - 1; j > start; --j) F = rescaled(ops.absorb_right(F.t, j, nullptr), F);
-    return F;
-  };
+  // Single layer: right-to-left half-sweeps contract each column once (rmid1 gives both the
+  // derivative and the new right environment); the double layer keeps the mid contraction
+  // from the left (its right-hand mirror has the same cost and cannot be reused: the
+  // environment needs the orthonormalised site, i.e. all of d, and the double-layer mid is
+  // too large to keep -- 137 GB per site at the metric shapes).
   for (int h = 0; h < nh; ++h) {
     if (h % 2 == 0) {
       for (int k = 0; k < K; ++k) {
-        Tensor E;
-        bool have_E = false;
         if (!(h > 0 && k == 0)) {
-          const bool want_E = dbl_reuse && k < K - 1;
-          Tensor d = ops.derivative(Lk[k].t, cols[k], Fk[k].t, want_E ? &E : nullptr);
-          have_E = want_E;
+          Tensor d = ops.derivative(Lk[k].t, cols[k], Fk[k].t);
           o[k] = view(d, o[k].shape);
           cl = Lk[k];
           cf = Fk[k];
@@ -527,28 +423,22 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
           nan_check(c, "F env", Fk[k].t, nb);
         }
         if (k < K - 1) {
-          Map mp;
-          o[k] = left_orth(c, o[k], nb, have_E ? &mp : nullptr);
-          Lk[k + 1] = (have_E && mp.valid) ? env_left_from(Lk[k], k, E, mp) : env_left(Lk[k], k);
+          o[k] = left_orth(c, o[k], nb);
+          Lk[k + 1] = env_left(Lk[k], k);
         }
       }
     } else {
       for (int k = K - 1; k >= 0; --k) {
-        Tensor E;
-        bool have_E = false;
         if (k != K - 1) {
-          const bool want_E = dbl_reuse && k > 0;
-          Tensor d = (s.dbl && !dbl_reuse) ? ops.derivative(Lk[k].t, cols[k], Fk[k].t)
-                                            : ops.derivative_right(Lk[k].t, cols[k], Fk[k].t, want_E ? &E : nullptr);
-          have_E = want_E;
+          Tensor d = s.dbl ? ops.derivative(Lk[k].t, cols[k], Fk[k].t)
+                           : ops.derivative_right(Lk[k].t, cols[k], Fk[k].t);
           o[k] = view(d, o[k].shape);
           cl = Lk[k];
           cf = Fk[k];
         }
         if (k > 0) {
-          Map mp;
-          o[k] = right_orth(c, o[k], nb, nullptr, have_E ? &mp : nullptr);
-          Fk[k - 1] = (have_E && mp.valid) ? env_right_from(Fk[k], k, E, mp) : env_right(Fk[k], k);
+          o[k] = right_orth(c, o[k], nb, nullptr);
+          Fk[k - 1] = env_right(Fk[k], k);
         }
       }
     }

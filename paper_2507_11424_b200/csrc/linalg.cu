@@ -842,36 +842,7 @@ static void gram(Ctx& c, const MatView& Y, const MatView& X, int m, int nb, bool
   TN_LAUNCHED();
 }
 
-// W[b] = W1[b] (times W2[b] where the second pass ran), FP64 -> complex FP32; full[b] = the
-// matrix had full numerical rank (no completion directions, Q = X W exactly).
-__global__ void __launch_bounds__(256) compose_w_kernel(const double2* __restrict__ W1, const double2* __restrict__ W2,
-                                                        const int* __restrict__ need2,
-                                                        const int* __restrict__ deficient, int n, float2* out,
-                                                        int* full) {
-  const int b = blockIdx.x;
-  const double2* A = W1 + (int64_t)b * n * n;
-  const double2* B2 = W2 + (int64_t)b * n * n;
-  float2* O = out + (int64_t)b * n * n;
-  const bool two = need2[b] != 0;
-  if (threadIdx.x == 0) full[b] = deficient[b] ? 0 : 1;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e - i * n;
-    double2 acc;
-    if (two) {
-      acc = make_double2(0, 0);
-      for (int k = 0; k < n; ++k) {
-        const double2 a = A[(int64_t)i * n + k], w = B2[(int64_t)k * n + j];
-        acc.x = fma(a.x, w.x, fma(-a.y, w.y, acc.x));
-        acc.y = fma(a.x, w.y, fma(a.y, w.x, acc.y));
-      }
-    } else {
-      acc = A[e];
-    }
-    O[e] = make_float2((float)acc.x, (float)acc.y);
-  }
-}
-
-static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, int nb, const OrthTransform* tr) {
+static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, int nb) {
   const int m = X.m, n = X.n;
   // kernel attributes are per device context: set once per device ordinal
   static std::atomic<uint64_t> attr_done{0};
@@ -906,11 +877,6 @@ static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, 
   if (always2) TN_CUDA(cudaMemsetAsync(need2, 0xFF, sizeof(int) * nb, c.stream));  // (-1: every matrix)
   apply64v_kernel<<<agrid, 256, 0, c.stream>>>(X, W.as<double2>(), Q1v, nullptr, need2, Q);
   TN_LAUNCHED();
-  DevBuf W1;
-  if (tr) {  // keep the first pass's map (W is overwritten below for deficient / second-pass matrices)
-    W1.alloc(nn * sizeof(double2), c.stream);
-    TN_CUDA(cudaMemcpyAsync(W1.p, W.p, nn * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream));
-  }
   // rank-deficient matrices only (every kernel returns at once for the others):
   // X' = [X P(:, :r), Y] -> Cholesky -> Q1 = X' R'^-1 (need2 is set for them)
   {
@@ -937,11 +903,6 @@ static void orth_fast(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, 
   TN_LAUNCHED();
   apply64v_kernel<<<agrid, 256, 0, c.stream>>>(Q1v, W.as<double2>(), Q, need2, nullptr, Q);
   TN_LAUNCHED();
-  if (tr) {
-    compose_w_kernel<<<nb, 256, 0, c.stream>>>(W1.as<double2>(), W.as<double2>(), need2, deficient, n, tr->W,
-                                               tr->full);
-    TN_LAUNCHED();
-  }
   if (Cout) {
     gram(c, Q, X, m, nb, false, nullptr, part, Gm.as<double2>());
     unsigned b2 = (unsigned)std::min<int64_t>(((int64_t)nn + 255) / 256, 4096);
@@ -1004,17 +965,16 @@ static void orth_check(Ctx& c, const MatView& X, const MatView& Q, int nb) {
   }
 }
 
-void orthonormalize(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, int nb, const OrthTransform* tr) {
+void orthonormalize(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, int nb) {
   int m = X.m, n = X.n;
   if (n == 0 || nb == 0) return;
   if (m < n) throw Error(-1, "orthonormalize: more columns than rows");
   ProfScope ps(P_ORTH, c.stream);
   if (n <= CH_MAXN && !getenv_flag("TN_ORTH_OLD")) {
-    orth_fast(c, X, Q, Cout, nb, tr);
+    orth_fast(c, X, Q, Cout, nb);
     if (getenv_flag("TN_ORTH_CHECK")) orth_check(c, X, Q, nb);
     return;
   }
-  if (tr) TN_CUDA(cudaMemsetAsync(tr->full, 0, sizeof(int) * nb, c.stream));  // no map on this path
   size_t nn = (size_t)n * n * nb;
   DevBuf G(nn * sizeof(double2), c.stream), W(nn * sizeof(double2), c.stream);
   DevBuf perm((size_t)n * nb * sizeof(int), c.stream), rank((size_t)nb * sizeof(int), c.stream);

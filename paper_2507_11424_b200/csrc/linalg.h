@@ -25,16 +25,6 @@ struct MatView {
 // Q(:, :) <- orthonormal basis of span(X) (n = X.n columns, requires X.m >= X.n), nb
 // matrices. If Cout is non-null it receives C = Q^H X as [b][n][n] complex FP32 (so that
 // X = Q C whenever span(X) is in span(Q)).
-//
-// If tr is non-null, it also receives the linear map of the full-rank matrices: Q = X W with
-// W [b][n][n] complex FP32 (row-major), and full[b] = 1 where W is valid (X of full numerical
-// rank, no completion directions), else 0 (device arrays). The fit uses it to obtain the new
-// environment from an accumulation against X itself instead of a second pass over the strip.
-struct OrthTransform {
-  float2* W = nullptr;
-  int* full = nullptr;
-};
-void orthonormalize(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, int nb,
-                    const OrthTransform* tr = nullptr);
+void orthonormalize(Ctx& c, const MatView& X, const MatView& Q, float2* Cout, int nb);
 
 }  // namespace tn
