@@ -41,15 +41,23 @@ def state_for(name):
     if recipe == "quench":
         path = os.path.join(GOLDEN, f"{name}_state.npz")
         if os.path.exists(path):
-            return lat, S.load_state(path)
+            return lat, load_p1_state(path)
         _, layers = G.CONFIGS["P1"][1], G.CONFIGS["P1"][3]
         st = G.heisenberg_quench(lat, chi, layers)
         st["tensors"] = [t.astype(np.complex64).astype(np.complex128) for t in st["tensors"]]
         meta = {k: v for k, v in st["meta"].items() if np.ndim(v) == 0}
         st["meta"] = dict(meta, rounded_to="complex64")
         S.save_state(path, st)
-        return lat, S.load_state(path)
+        z = dict(np.load(path))  # stored as complex64 (exact: the state is rounded to complex64)
+        np.savez_compressed(path, **{k: (v.astype(np.complex64) if v.dtype == np.complex128 else v) for k, v in z.items()})
+        return lat, load_p1_state(path)
     return lat, S.vidal_like(lat, chi, seed=2507)
+
+
+def load_p1_state(path):
+    st = S.load_state(path)
+    st["tensors"] = [np.asarray(t, dtype=np.complex128) for t in st["tensors"]]
+    return st
 
 
 def main(name):

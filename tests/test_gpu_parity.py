@@ -347,3 +347,49 @@ def test_degenerate_partitions_vs_statevector(shape, order):
     for k in range(4):
         idx = int("".join(map(str, bits[k])), 2)
         assert abs(la[k] - math.log(abs(psi[idx]))) < 1e-4
+
+
+# ------------------------------------------------------------------ oracle goldens (P1, w16)
+GOLDEN = __import__("os").path.join(__import__("os").path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    import os
+    path = os.path.join(GOLDEN, f"{name}_oracle.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated (scripts/make_golden.py {name})")
+    return np.load(path)
+
+
+def test_p1_willow_quench_vs_oracle_golden():
+    """P1 (SURVEY 8(d) parity aux): Willow-105, L = 15 domain-wall Heisenberg quench at chi = 8
+    (the oracle generator's state rounded to complex64, tests/golden/p1_state.npz), chi_env = 32,
+    64 samples: every conditional, ln q and bit against the CPU oracle's values
+    (tests/golden/p1_oracle.npz, written by scripts/make_golden.py p1 -- oracle/ only), at R16."""
+    import os
+    ref = _golden("p1")
+    st = S.load_state(os.path.join(GOLDEN, "p1_state.npz"))
+    st["tensors"] = [np.asarray(t, dtype=np.complex128) for t in st["tensors"]]
+    lat = L.willow105()
+    R = int(ref["chi_env"])
+    u = S.uniforms(len(ref["logq"]), lat.n, int(ref["uniform_seed"]))
+    g, bits, logq, cond, flags = _run(st, lat.rows, R, u)
+    rep = compare_samples(order_of(lat.rows), u, bits, logq, cond, ref["bits"], ref["logq"], ref["cond"])
+    print("P1", rep)
+    assert rep["compared"] >= 60 * lat.n
+    assert abs(g.log_norm(R) - float(ref["log_norm"])) <= 1e-4 * abs(float(ref["log_norm"]))
+
+
+def test_w16_willow_vs_oracle_golden():
+    """Willow-105 at chi = 16, chi_env = 64 (Vidal-like state of the bench's recipe, seed 2507):
+    the GPU against the CPU oracle's conditionals, ln q and bits (tests/golden/w16_oracle.npz,
+    scripts/make_golden.py w16), at R16."""
+    ref = _golden("w16")
+    lat = L.willow105()
+    st = S.vidal_like(lat, int(ref["chi"]), seed=2507)
+    R = int(ref["chi_env"])
+    u = S.uniforms(len(ref["logq"]), lat.n, int(ref["uniform_seed"]))
+    g, bits, logq, cond, flags = _run(st, lat.rows, R, u)
+    rep = compare_samples(order_of(lat.rows), u, bits, logq, cond, ref["bits"], ref["logq"], ref["cond"])
+    print("w16", rep)
+    assert rep["compared"] >= (len(u) - 1) * lat.n
