@@ -43,6 +43,9 @@ WORKLOADS = {
     "square6x6_chi8_env32": ("square6x6", 8, 32, 512),
     # the paper's literal order is meant for chi_env <= chi (R <= 20 with chi >= 20)
     "willow105_chi8_env8": ("willow105", 8, 8, 256),
+    # config 5 shapes (LUCJ-like two-register ladders, rows = rung pairs, chi = 64, chi_env = 256)
+    "lucj52_chi64_env256": ("lucj52", 64, 256, 64),
+    "lucj72_chi64_env256": ("lucj72", 64, 256, 64),
 }
 PHASES = ["gemm_tc_incl_prep", "gemm_simt", "permute", "orth", "tail", "misc", "tc_kernel"]
 DEFAULT_WORKLOAD = "willow105_chi32_env128"

@@ -96,6 +96,18 @@ int tn_sample_dev(tn_state* st, const int32_t* row_ptr, const int32_t* row_verti
                   int32_t chi_env, int64_t n_samples, const double* uniforms_dev, uint8_t* out_bits_dev,
                   double* out_logp_dev, double* out_cond_dev, uint32_t* out_flags_dev, void* stream);
 
+/* tn_sample plus the amplitude carried along each sample's own sampling path (PAPER.md:293:
+ * "if the MPS dimension R_x used is large enough such that only minimal truncations are made
+ * in the fitting procedures ... [p(x)] is the square of the MPS-MPS contraction
+ * m_{N_b-1 -> N_b} . X_{N_b}"): out_logabs[k] = ln|a_k|, out_phase[k] = arg a_k, where a_k is
+ * the product of the row fits' norms, the merge normalisations and the final scalar of the
+ * projected rows; p(x_k) ~ |a_k|^2 (exact when no fit truncates, else an approximation --
+ * tn_certify gives the independent contraction). Host arrays [n_samples]; compress-then-sample
+ * order only (TN_E_ARG under option order = 1). Other arguments and errors as tn_sample. */
+int tn_sample_path(tn_state* st, const int32_t* row_ptr, const int32_t* row_vertices, int32_t n_rows,
+                   int32_t chi_env, int64_t n_samples, const double* uniforms, uint8_t* out_bits,
+                   double* out_logq, double* out_logabs, double* out_phase);
+
 /* Amplitudes <x|psi> (D3) of n bitstrings bits[k][v] (by vertex id), contracted by
  * boundary MPS of bond <= chi_env over the state's current row order (the last one given to
  * tn_prepare / tn_sample; TN_E_ROWS if none) ("separate contraction of
@@ -132,6 +144,25 @@ typedef struct {
 } tn_cert_stats;
 int tn_certify(tn_state* st, const uint8_t* bits, const double* logq, int64_t n, int32_t chi_env_verify,
                double log_z, double* out_logp, tn_cert_stats* out);
+
+/* Sample observables ("importance sampling" formula;
+ * PAPER.md:174 magnetisation pass rate). For n samples bits[k][v] (host, [n][n_vertices]) with
+ * ln q (sampled, from tn_sample) and ln p (from tn_certify or tn_sample_path), on the current
+ * device:
+ *   out_z_weighted[v] = sum_k w_k z_v(x_k) / sum_k w_k, w_k = p_k / q_k, z_v = 1 - 2 x_v: the
+ *                       importance-sampled <psi|Z_v|psi> / <psi|psi> (self-normalised, N = the
+ *                       mean ratio as in P:299-300); samples with a non-finite ratio weigh 0;
+ *   out_z_plain[v]    = (1/n) sum_k z_v(x_k) (the uncorrected sample mean under q);
+ *   out_pass_rate     = fraction of samples whose number of ones in each group g
+ *                       (group_of[v] in [0, n_groups), -1 = no group) equals target_ones[g]
+ *                       (the magnetisation / particle-number sector; n_groups = 0 -> 1);
+ *   out_pass_rate_weighted (optional) = the same fraction with the importance weights.
+ * Sums are in FP64 with a fixed reduction order (deterministic). n_groups <= 8.
+ * Errors: TN_E_ARG (NULL, n <= 0, n_groups out of range), TN_E_CUDA. */
+int tn_observables(const uint8_t* bits, const double* logq, const double* logp, int64_t n, int32_t n_vertices,
+                   const int32_t* group_of, int32_t n_groups, const int32_t* target_ones,
+                   double* out_z_weighted, double* out_z_plain, double* out_pass_rate,
+                   double* out_pass_rate_weighted);
 
 /* Options (SURVEY 5 "Config / flags"): "fit_half_sweeps" (nh, default 2, R5), "init_seed"
  * (default 0x2507114240, R4), "gemm" (0 = auto, 1 = force SIMT FP32, 2 = force tcgen05

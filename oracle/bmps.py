@@ -373,9 +373,10 @@ def _n_strip(P: Prepared, b, m_prev):
     return Strip("single", tops, mats, [True] * len(row))
 
 
-def _merge(P: Prepared, row, sites):
+def _merge(P: Prepared, row, sites, norms=None):
     """a5 / R14: slice s = x_v (done by the caller), multiply every vertex without a
-    down-edge into the nearest down-edge site to its right, else to its left; normalise."""
+    down-edge into the nearest down-edge site to its right, else to its left; normalise
+    (the norms divided out are appended to `norms` when given)."""
     downs = [j for j, v in enumerate(row) if P.has(v, "down")]
     if not downs:
         return None
@@ -391,17 +392,33 @@ def _merge(P: Prepared, row, sites):
                 mat = sites[i][:, 0, :]
                 t = np.tensordot(t, mat, axes=([2], [0]))
         prev = j
-        out.append(t / np.linalg.norm(t))
+        nrm = np.linalg.norm(t)
+        if norms is not None:
+            norms.append(nrm)
+        out.append(t / nrm)
     return out
 
 
+def _row_scalar(sites):
+    """Product of the projected sites [a, 1, b] of a row without down edges: the scalar the
+    boundary contraction ends in (m_{N_b - 1 -> N_b} . X_{N_b})."""
+    t = sites[0][:, 0, :]
+    for x in sites[1:]:
+        t = t @ x[:, 0, :]
+    return complex(t.reshape(-1)[0])
+
+
 def sample(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2, forced=None, max_rows=None,
-           first_row=0, m_in=None):
+           first_row=0, m_in=None, path_amplitude=False):
     """O5 for one sample: returns (bits[N] uint8 by vertex id, ln q, cond[N], flags).
     With `forced` (bits by vertex id) the draw is replaced by the given bits, which
     evaluates q(x) of any x (used to enumerate the whole distribution in tests).
     first_row / m_in / max_rows run rows first_row .. max_rows-1 only, starting from the
     incoming boundary MPS m_in (bounded CPU timing of a part of a sample only).
+    path_amplitude: also return (ln|a|, arg a) of the amplitude carried along the sampling
+    path, a = prod_b ||Fit(m_{b-1} psi_b)|| * ||merge(n_b[x_b])|| * (final scalar), i.e. the
+    MPS-MPS contraction m_{N_b-1 -> N_b} . X_{N_b} whose square is p(x) when the fits are
+    (near) exact (the first of its two ways to obtain p).
 
     Row b: n_b = Fit_R(m_{b-1} . psi_b) with (s, d) open (R3 compress-then-sample); right
     ladder R^(s)_j = n_j[s] M_j conj(n_j[s]) R_{j+1}; left pass w_s = Re<L_j, R^(s)_j>,
@@ -413,13 +430,15 @@ def sample(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2,
     logq = 0.0
     flags = 0
     m_prev = m_in
+    log_amp, phase = 0.0, 0.0
     for b, row in enumerate(P.rows):
         if b < first_row:
             continue
         if max_rows is not None and b >= max_rows:  # partial run (bounded CPU timing only)
             break
         strip = _n_strip(P, b, m_prev)
-        nsites, _ = fit(strip, R, TAG_N, b + 1, seed, nh)
+        nsites, n_lg = fit(strip, R, TAG_N, b + 1, seed, nh)
+        log_amp += n_lg
         W = len(row)
         ns = []
         for j, v in enumerate(row):
@@ -466,7 +485,15 @@ def sample(P: Prepared, M, R: int, u_row, seed: int = DEFAULT_SEED, nh: int = 2,
             if scale > 0:
                 Lx = Lx / scale
         proj = [ns[j][:, bits[v]] for j, v in enumerate(row)]
-        m_prev = _merge(P, row, proj)
+        norms = []
+        m_prev = _merge(P, row, proj, norms)
+        log_amp += sum(math.log(x) if x > 0 else -math.inf for x in norms)
+        if m_prev is None:  # no down edges: the boundary contraction ends in a scalar
+            sc = _row_scalar(proj)
+            log_amp += math.log(abs(sc)) if sc != 0 else -math.inf
+            phase = math.atan2(sc.imag, sc.real)
+    if path_amplitude:
+        return bits, logq, cond, flags, (log_amp, phase)
     return bits, logq, cond, flags
 
 

@@ -178,6 +178,53 @@ def heisenberg_quench(lat, chi: int, layers: int, J: float = 1.0, dt: float = 0.
                             "bp_residual_max": float(max(residuals) if residuals else 0.0)})
 
 
+def lucj_circuit(lat, chi: int, n_occ: int, rot_layers: int, seed: int):
+    """Synthetic LUCJ-like circuit on a two-register ladder (config 5, SURVEY 8(d), R22;
+    PAPER.md:147-151: "particle number preserving rotations - most prominently
+    controlled-phase gates and XX + YY rotations"; the real circuits are not public,
+    PAPER.md:234). Initial state HF-like: the first n_occ qubits of each register |1>, the
+    rest |0> (R18-style reconstruction). Circuit: rot_layers brickwork layers of XX+YY(theta)
+    on both register chains (even bonds, then odd bonds; an orbital-rotation network), one
+    CP(phi) layer on every rung (the Jastrow part: "one or two control-phase gates per
+    sub-register connection", PAPER.md:155), rot_layers more brickwork layers;
+    theta, phi ~ U[-pi, pi) from default_rng(seed). BP refresh before every layer of
+    non-overlapping gates."""
+    n_reg = lat.n // 2
+    bits = [1 if (v // 2) < n_occ else 0 for v in range(lat.n)]
+    tns = TNS(lat, bits)
+    rng = np.random.default_rng(seed)
+    chain = {}
+    rungs = []
+    for e, (u, v) in enumerate(lat.edges):
+        if v - u == 2:
+            chain[(u, v)] = e
+        else:
+            rungs.append(e)
+    alpha = [chain[(2 * i, 2 * i + 2)] for i in range(n_reg - 1)]
+    beta = [chain[(2 * i + 1, 2 * i + 3)] for i in range(n_reg - 1)]
+    residuals = []
+
+    def rot_layer():
+        for parity in (0, 1):
+            group = [e for i, e in enumerate(alpha) if i % 2 == parity] + \
+                    [e for i, e in enumerate(beta) if i % 2 == parity]
+            residuals.append(tns.bp())
+            for e in group:
+                tns.apply2(e, xxpyy_gate(rng.uniform(-np.pi, np.pi)), chi)
+
+    for _ in range(rot_layers):
+        rot_layer()
+    residuals.append(tns.bp())
+    for e in rungs:
+        tns.apply2(e, cphase_gate(rng.uniform(-np.pi, np.pi)), chi)
+    for _ in range(rot_layers):
+        rot_layer()
+    n_gates = 2 * rot_layers * (len(alpha) + len(beta))
+    return tns.state(chi, {"kind": "lucj", "n_occ": n_occ, "rot_layers": rot_layers, "seed": seed,
+                           "n_xxpyy": n_gates, "n_cp": len(rungs),
+                           "bp_residual_max": float(max(residuals) if residuals else 0.0)})
+
+
 CONFIGS = {
     # name: (lattice, chi, chi_env, layers, n_samples, uniform_seed)   SURVEY 8(d)
     "cfg1": ("square3x3", 4, 16, 2, 1024, 1001),
@@ -186,10 +233,21 @@ CONFIGS = {
     "cfg4a": ("willow105", 32, 128, 7, 100000, 1004),
     "cfg4b": ("willow105", 32, 128, 15, 100000, 1005),
     "P1": ("willow105", 8, 32, 15, 1000, 1008),
+    # LUCJ-like (rot_layers brickwork layers before and after the CP layer; 13 + 13 layers
+    # give 1300 / 1820 XX+YY rotations on 52 / 72 qubits, "~1800")
+    "cfg5a": ("lucj52", 64, 256, 13, 100000, 1006),
+    "cfg5b": ("lucj72", 64, 256, 13, 100000, 1007),
 }
+LUCJ = {"cfg5a": (5, 2006), "cfg5b": (27, 2007)}  # (HF-like occupation per register, circuit seed)
 
 
-def config_state(name: str):
-    lat_name, chi, _, layers, _, _ = CONFIGS[name]
+def config_state(name: str, chi: int = None, layers: int = None):
+    """The state of a SURVEY 8(d) configuration (optionally at another chi / depth)."""
+    lat_name, chi0, _, layers0, _, _ = CONFIGS[name]
     lat = L.by_name(lat_name)
+    chi = chi0 if chi is None else chi
+    layers = layers0 if layers is None else layers
+    if name in LUCJ:
+        n_occ, seed = LUCJ[name]
+        return lat, lucj_circuit(lat, chi, n_occ, layers, seed)
     return lat, heisenberg_quench(lat, chi, layers)

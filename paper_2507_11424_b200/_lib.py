@@ -16,8 +16,9 @@ LIB_PATH = os.path.join(HERE, "libtnsample.so")
 TN_OK = 0
 ERRORS = {-1: "TN_E_ARG", -2: "TN_E_GRAPH", -3: "TN_E_ROWS", -4: "TN_E_NOMEM", -5: "TN_E_CUDA",
           -6: "TN_E_NCCL", -7: "TN_E_NUMERIC"}
-EXPORTS = ["tn_load_state", "tn_prepare", "tn_sample", "tn_sample_ex", "tn_sample_dev", "tn_amplitude",
-           "tn_log_norm", "tn_certify", "tn_set_option", "tn_get_stats", "tn_free_state", "tn_last_error"]
+EXPORTS = ["tn_load_state", "tn_prepare", "tn_sample", "tn_sample_ex", "tn_sample_dev", "tn_sample_path",
+           "tn_amplitude", "tn_log_norm", "tn_certify", "tn_observables", "tn_set_option", "tn_get_stats",
+           "tn_free_state", "tn_last_error"]
 
 
 class TNError(RuntimeError):
@@ -48,6 +49,8 @@ def load_library(path: str = LIB_PATH):
     lib.tn_sample.argtypes = [P, i32p, i32p, C.c_int32, C.c_int32, C.c_int64, P, P, P]
     lib.tn_sample_ex.argtypes = [P, i32p, i32p, C.c_int32, C.c_int32, C.c_int64, C.c_int64, P, P, P, P, P]
     lib.tn_sample_dev.argtypes = [P, i32p, i32p, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P]
+    lib.tn_sample_path.argtypes = [P, i32p, i32p, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P]
+    lib.tn_observables.argtypes = [P, P, P, C.c_int64, C.c_int32, P, C.c_int32, P, P, P, P, P]
     lib.tn_amplitude.argtypes = [P, P, C.c_int64, C.c_int32, P, P]
     lib.tn_log_norm.argtypes = [P, C.c_int32, C.POINTER(C.c_double)]
     lib.tn_certify.argtypes = [P, P, P, C.c_int64, C.c_int32, C.c_double, P, C.POINTER(CertStats)]
@@ -150,6 +153,20 @@ class TNState:
                                    C.c_void_p(bits_ptr), C.c_void_p(logp_ptr), C.c_void_p(cond_ptr or None),
                                    C.c_void_p(flags_ptr or None), C.c_void_p(stream or None)))
 
+    def sample_path(self, rows, chi_env: int, uniforms):
+        """tn_sample_path: bits, ln q and the amplitude carried along each sample's sampling path
+        (ln|a|, arg a; p ~ |a|^2 when the fits are near exact)."""
+        u = np.ascontiguousarray(uniforms, dtype=np.float64)
+        n = u.shape[0]
+        bits = np.zeros((n, self.n), dtype=np.uint8)
+        logq = np.zeros(n)
+        la = np.zeros(n)
+        ph = np.zeros(n)
+        p, v, nr, *_keep = self._csr(rows)
+        _check(lib().tn_sample_path(self._h, p, v, nr, int(chi_env), n, _ptr(u), _ptr(bits), _ptr(logq), _ptr(la),
+                                    _ptr(ph)))
+        return bits, logq, la, ph
+
     def amplitude(self, bits, chi_env: int):
         b = np.ascontiguousarray(bits, dtype=np.uint8)
         n = b.shape[0]
@@ -179,3 +196,27 @@ class TNState:
         t = C.c_double()
         _check(lib().tn_get_stats(self._h, C.byref(n), C.byref(t)))
         return {"launches": n.value, "precompute_s": t.value}
+
+
+def observables(bits, logq, logp, groups=None, targets=None):
+    """tn_observables (NEXT-1): importance-sampled <Z_v>, the plain
+    sample mean of Z_v, and the sector pass rate (plain and weighted). groups: [N] group id per
+    vertex (-1 = none) with targets[g] = required number of ones in group g."""
+    b = np.ascontiguousarray(bits, dtype=np.uint8)
+    n, N = b.shape
+    q = np.ascontiguousarray(logq, dtype=np.float64)
+    lp = np.ascontiguousarray(logp, dtype=np.float64)
+    zw = np.zeros(N)
+    zp = np.zeros(N)
+    pr = C.c_double()
+    prw = C.c_double()
+    if groups is None:
+        g = t = None
+        ng = 0
+    else:
+        g = np.ascontiguousarray(groups, dtype=np.int32)
+        t = np.ascontiguousarray(targets, dtype=np.int32)
+        ng = len(t)
+    _check(lib().tn_observables(_ptr(b), _ptr(q), _ptr(lp), n, N, _ptr(g), ng, _ptr(t), _ptr(zw), _ptr(zp),
+                                C.byref(pr), C.byref(prw)))
+    return {"z_weighted": zw, "z_plain": zp, "pass_rate": pr.value, "pass_rate_weighted": prw.value}

@@ -295,6 +295,23 @@ void log_add(Ctx& c, double* out, const double* a, const double* b, const double
   TN_LAUNCHED();
 }
 
+namespace {
+__global__ void scalar_logphase_kernel(const float2* __restrict__ t, int64_t bs, int nb, double* logacc,
+                                       double* phase) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const float2 v = t[b * bs];
+  const double a = hypot((double)v.x, (double)v.y);
+  logacc[b] += a > 0 ? log(a) : -INFINITY;
+  phase[b] = atan2((double)v.y, (double)v.x);
+}
+}  // namespace
+
+void scalar_logphase(Ctx& c, const Tensor& t, int nb, double* logacc, double* phase) {
+  scalar_logphase_kernel<<<ceil_div(nb, 128), 128, 0, c.stream>>>(t.p, t.bstride, nb, logacc, phase);
+  TN_LAUNCHED();
+}
+
 void scalars_to_host(Ctx& c, const Tensor& t, int nb, std::vector<float2>& out) {
   out.resize(nb);
   int n = t.bstride ? nb : 1;
@@ -403,7 +420,87 @@ __global__ void __launch_bounds__(1024) cert_kernel(const double* __restrict__ l
     out[5] = (double)n - cnt;
   }
 }
+// Importance weights w_k = exp(ln p_k - ln q_k - max) (0 for non-finite ratios) and the
+// per-sample sector test: pass[k] = every group g holds target[g] ones (1 if no groups).
+__global__ void __launch_bounds__(1024) obs_weights_kernel(const double* __restrict__ lq, const double* __restrict__ lp,
+                                                          const uint8_t* __restrict__ bits, int64_t n, int N,
+                                                          const int* __restrict__ group_of, int n_groups,
+                                                          const int* __restrict__ target, double* __restrict__ w,
+                                                          double* __restrict__ pass) {
+  __shared__ double red[32];
+  __shared__ double s_mx;
+  const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+  double mx = -INFINITY;
+  for (int64_t k = t; k < n; k += blockDim.x) {
+    const double d = lp[k] - lq[k];
+    if (isfinite(d)) mx = fmax(mx, d);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[wp] = mx;
+  __syncthreads();
+  if (t == 0) {
+    double x = -INFINITY;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) x = fmax(x, red[i]);
+    s_mx = x;
+  }
+  __syncthreads();
+  for (int64_t k = t; k < n; k += blockDim.x) {
+    const double d = lp[k] - lq[k];
+    w[k] = isfinite(d) ? exp(d - s_mx) : 0.0;
+    int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (group_of)
+      for (int v = 0; v < N; ++v) {
+        const int g = group_of[v];
+        if (g >= 0 && g < 8) cnt[g] += bits[k * N + v];
+      }
+    bool ok = true;
+    for (int g = 0; g < n_groups && g < 8; ++g) ok = ok && cnt[g] == target[g];
+    pass[k] = ok ? 1.0 : 0.0;
+  }
+}
+
+// Block v: fixed-order sums over the samples of w z_v, z_v, w (z = 1 - 2 x_v) and, in block N,
+// of pass and w pass (deterministic: per-thread strided partial sums, fixed tree).
+__global__ void __launch_bounds__(256) obs_sums_kernel(const uint8_t* __restrict__ bits, const double* __restrict__ w,
+                                                      const double* __restrict__ pass, int64_t n, int N,
+                                                      double* __restrict__ out) {
+  __shared__ double sh[3][256];
+  const int v = blockIdx.x, t = threadIdx.x;
+  double a = 0, b = 0, c = 0;
+  for (int64_t k = t; k < n; k += blockDim.x) {
+    if (v < N) {
+      const double z = 1.0 - 2.0 * bits[k * N + v];
+      a += w[k] * z;
+      b += z;
+      c += w[k];
+    } else {
+      a += pass[k];
+      b += w[k] * pass[k];
+      c += w[k];
+    }
+  }
+  sh[0][t] = a;
+  sh[1][t] = b;
+  sh[2][t] = c;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (t < s)
+      for (int q = 0; q < 3; ++q) sh[q][t] += sh[q][t + s];
+    __syncthreads();
+  }
+  if (t == 0)
+    for (int q = 0; q < 3; ++q) out[3 * v + q] = sh[q][0];
+}
 }  // namespace
+
+void observables(Ctx& c, const uint8_t* bits, const double* logq, const double* logp, int64_t n, int N,
+                 const int* group_of, int n_groups, const int* target, double* w, double* pass, double* sums) {
+  obs_weights_kernel<<<1, 1024, 0, c.stream>>>(logq, logp, bits, n, N, group_of, n_groups, target, w, pass);
+  TN_LAUNCHED();
+  obs_sums_kernel<<<N + 1, 256, 0, c.stream>>>(bits, w, pass, n, N, sums);
+  TN_LAUNCHED();
+}
+
 void cert_stats(Ctx& c, const double* logq, const double* logp, int64_t n, double log_z, double* out) {
   cert_kernel<<<1, 1024, 0, c.stream>>>(logq, logp, n, log_z, out);
   TN_LAUNCHED();

@@ -10,6 +10,10 @@ void hash_init(Ctx& c, Tensor& o, int nb, uint64_t seed, int tag, int b1, int k)
 // Per-sample Frobenius norm: t <- t / ||t||, logn[b] (+)= ln ||t|| when logn != nullptr.
 // tn_certify statistics: out[0..5] = ln mean(p/q), rel. stderr, KLD, ESS, n used, n excluded
 void cert_stats(Ctx& c, const double* logq, const double* logp, int64_t n, double log_z, double* out);
+// tn_observables: importance weights w [n] (relative, max 1), sector indicators pass [n] and
+// sums [3 (N+1)]: for v < N (sum w z_v, sum z_v, sum w), then (sum pass, sum w pass, sum w).
+void observables(Ctx& c, const uint8_t* bits, const double* logq, const double* logp, int64_t n, int N,
+                 const int* group_of, int n_groups, const int* target, double* w, double* pass, double* sums);
 int64_t count_nonfinite(Ctx& c, const float2* p, int64_t n);  // debugging (synchronises)
 void normalize(Ctx& c, Tensor& t, int nb, double* logn, bool accumulate_log);
 
@@ -47,6 +51,9 @@ void add_into(Ctx& c, Tensor& dst, const Tensor& src, int nb);
 
 // out[i] = (acc ? out[i] : 0) + a[i] + (b ? b[i] : 0) + (c ? c[i] : 0), i < n (device arrays)
 void log_add(Ctx& c, double* out, const double* a, const double* b, const double* c2, int n, bool acc);
+
+// Per-sample scalar t[b][0]: logacc[b] += ln|t|, phase[b] = arg t (device arrays).
+void scalar_logphase(Ctx& c, const Tensor& t, int nb, double* logacc, double* phase);
 
 // out[b] = per-sample scalar t[b][0] -> host (complex) helper
 void scalars_to_host(Ctx& c, const Tensor& t, int nb, std::vector<float2>& out);

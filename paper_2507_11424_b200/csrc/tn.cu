@@ -295,14 +295,22 @@ int64_t per_sample_bytes(const Layout& L, int R, int chi) {
 }
 
 // O5 for one batch of nb samples (device outputs).
+// pa_log / pa_phase (optional, device [nb]): ln|a| and arg a of the amplitude carried along
+// the sampling path (m_{N_b-1 -> N_b} . X_{N_b}; p(x) = |a|^2 when the fits
+// are (near) exact): the n-fits' log-norms, the merge normalisations and the final scalar.
 void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double* u_dev, uint8_t* bits_dev,
-                  double* logq_dev, double* cond_dev, uint32_t* flags_dev) {
+                  double* logq_dev, double* cond_dev, uint32_t* flags_dev, double* pa_log = nullptr,
+                  double* pa_phase = nullptr) {
   Ctx& c = st->ctx;
   c.nb = nb;
   int N = st->n;
   TN_CUDA(cudaMemsetAsync(logq_dev, 0, sizeof(double) * nb, c.stream));
   TN_CUDA(cudaMemsetAsync(flags_dev, 0, sizeof(uint32_t) * nb, c.stream));
   DevBuf xbuf(sizeof(int) * nb, c.stream);
+  if (pa_log) {
+    TN_CUDA(cudaMemsetAsync(pa_log, 0, sizeof(double) * nb, c.stream));
+    TN_CUDA(cudaMemsetAsync(pa_phase, 0, sizeof(double) * nb, c.stream));
+  }
   std::vector<Tensor> m_prev;
   bool have_prev = false;
   g_row_cmacs.assign(L.rows.size(), 0.0);
@@ -325,7 +333,7 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
       s.mats.push_back(L.Bn[v]);
       s.out.push_back(true);
     }
-    FitResult fr = fit(c, s, R, 1, b + 1, st->seed, st->nh, nullptr, false);
+    FitResult fr = fit(c, s, R, 1, b + 1, st->seed, st->nh, pa_log, pa_log != nullptr);
     for (int j = 0; j < W; ++j) nan_check(c, ("n site row " + std::to_string(b) + " j " + std::to_string(j)).c_str(), fr.sites[j], nb);
     std::vector<Tensor> n(W);
     for (int j = 0; j < W; ++j) {
@@ -379,6 +387,14 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
       if (has(L, row[j], 1)) downs.push_back(j);
     m_prev.clear();
     have_prev = !downs.empty();
+    if (downs.empty() && pa_log) {  // the boundary contraction ends in a scalar
+      Tensor t = viewt(proj[0], {proj[0].shape[0], proj[0].shape[2]});
+      for (int i = 1; i < W; ++i) {
+        Tensor mat = viewt(proj[i], {proj[i].shape[0], proj[i].shape[2]});
+        t = contract(c, t, "ab", false, mat, "bc", false, "ac");
+      }
+      scalar_logphase(c, t, nb, pa_log, pa_phase);
+    }
     int prev = -1;
     for (size_t k = 0; k < downs.size(); ++k) {
       int j = downs[k];
@@ -392,7 +408,7 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
           Tensor mat = viewt(proj[i], {proj[i].shape[0], proj[i].shape[2]});
           t = contract(c, t, "adz", false, mat, "zy", false, "ady");
         }
-      normalize(c, t, nb, nullptr, false);
+      normalize(c, t, nb, pa_log, pa_log != nullptr);
       m_prev.push_back(t);
       prev = j;
     }
@@ -559,7 +575,8 @@ void use_device(tn_state* st) { TN_CUDA(cudaSetDevice(st->device)); }
 
 void sample_common(tn_state* st, const int32_t* row_ptr, const int32_t* rv, int32_t n_rows, int32_t chi_env,
                    int64_t n_samples, const double* u, bool u_on_device, uint8_t* bits, double* logp, double* cond,
-                   uint32_t* flags, bool out_on_device, cudaStream_t user_stream) {
+                   uint32_t* flags, bool out_on_device, cudaStream_t user_stream, double* pa_log = nullptr,
+                   double* pa_phase = nullptr) {
   if (!st) throw Error(TN_E_ARG, "state is NULL");
   if (n_samples <= 0) throw Error(TN_E_ARG, "n_samples must be > 0");
   if (chi_env < 1) throw Error(TN_E_ARG, "chi_env must be >= 1");
@@ -612,8 +629,19 @@ void sample_common(tn_state* st, const int32_t* row_ptr, const int32_t* rv, int3
         fd = fb.as<uint32_t>();
         cd = cond ? cb.as<double>() : nullptr;
       }
+      DevBuf pal, pap;  // path amplitudes (host outputs only)
+      if (pa_log) {
+        if (out_on_device || st->order == 1) throw Error(TN_E_ARG, "path amplitudes: host outputs, order 0 only");
+        pal.alloc(sizeof(double) * nb, c.stream);
+        pap.alloc(sizeof(double) * nb, c.stream);
+      }
       if (st->order == 1) sample_batch_literal(st, L, E, chi_env, nb, ud, bd, ld, cd, fd);
-      else sample_batch(st, L, E, chi_env, nb, ud, bd, ld, cd, fd);
+      else sample_batch(st, L, E, chi_env, nb, ud, bd, ld, cd, fd, pa_log ? pal.as<double>() : nullptr,
+                        pa_log ? pap.as<double>() : nullptr);
+      if (pa_log) {
+        TN_CUDA(cudaMemcpyAsync(pa_log + done, pal.p, sizeof(double) * nb, cudaMemcpyDeviceToHost, c.stream));
+        TN_CUDA(cudaMemcpyAsync(pa_phase + done, pap.p, sizeof(double) * nb, cudaMemcpyDeviceToHost, c.stream));
+      }
       if (!out_on_device) {
         TN_CUDA(cudaMemcpyAsync(bits + done * N, bd, (size_t)nb * N, cudaMemcpyDeviceToHost, c.stream));
         TN_CUDA(cudaMemcpyAsync(logp + done, ld, sizeof(double) * nb, cudaMemcpyDeviceToHost, c.stream));
@@ -766,6 +794,16 @@ int tn_sample_ex(tn_state* st, const int32_t* row_ptr, const int32_t* row_vertic
   });
 }
 
+int tn_sample_path(tn_state* st, const int32_t* row_ptr, const int32_t* row_vertices, int32_t n_rows,
+                   int32_t chi_env, int64_t n_samples, const double* uniforms, uint8_t* out_bits, double* out_logq,
+                   double* out_logabs, double* out_phase) {
+  return guarded([&] {
+    if (!out_logabs || !out_phase) throw Error(TN_E_ARG, "NULL path-amplitude output");
+    sample_common(st, row_ptr, row_vertices, n_rows, chi_env, n_samples, uniforms, false, out_bits, out_logq,
+                  nullptr, nullptr, false, nullptr, out_logabs, out_phase);
+  });
+}
+
 int tn_sample_dev(tn_state* st, const int32_t* row_ptr, const int32_t* row_vertices, int32_t n_rows, int32_t chi_env,
                   int64_t n_samples, const double* uniforms_dev, uint8_t* out_bits_dev, double* out_logp_dev,
                   double* out_cond_dev, uint32_t* out_flags_dev, void* stream) {
@@ -864,6 +902,51 @@ int tn_certify(tn_state* st, const uint8_t* bits, const double* logq, int64_t n,
     out->n_used = (int64_t)h[4];
     out->n_excluded = (int64_t)h[5];
     if (out_logp) std::copy(lp.begin(), lp.end(), out_logp);
+  });
+}
+
+int tn_observables(const uint8_t* bits, const double* logq, const double* logp, int64_t n, int32_t n_vertices,
+                   const int32_t* group_of, int32_t n_groups, const int32_t* target_ones, double* out_z_weighted,
+                   double* out_z_plain, double* out_pass_rate, double* out_pass_rate_weighted) {
+  return guarded([&] {
+    if (!bits || !logq || !logp || !out_z_weighted || !out_z_plain || !out_pass_rate)
+      throw Error(TN_E_ARG, "NULL argument");
+    if (n <= 0 || n_vertices < 1) throw Error(TN_E_ARG, "n and n_vertices must be > 0");
+    if (n_groups < 0 || n_groups > 8 || (n_groups > 0 && (!group_of || !target_ones)))
+      throw Error(TN_E_ARG, "n_groups must be in [0, 8] with group_of and target_ones given");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) throw Error(TN_E_CUDA, "no CUDA device");
+    Ctx c;
+    TN_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{c.stream};
+    const int N = n_vertices;
+    {
+      DevBuf db((size_t)n * N, c.stream), dq(sizeof(double) * n, c.stream), dp(sizeof(double) * n, c.stream);
+      DevBuf dw(sizeof(double) * n, c.stream), dpass(sizeof(double) * n, c.stream);
+      DevBuf ds(sizeof(double) * 3 * (N + 1), c.stream), dg(sizeof(int) * N, c.stream), dt(sizeof(int) * 8, c.stream);
+      TN_CUDA(cudaMemcpyAsync(db.p, bits, (size_t)n * N, cudaMemcpyHostToDevice, c.stream));
+      TN_CUDA(cudaMemcpyAsync(dq.p, logq, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      TN_CUDA(cudaMemcpyAsync(dp.p, logp, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      if (n_groups > 0) {
+        TN_CUDA(cudaMemcpyAsync(dg.p, group_of, sizeof(int) * N, cudaMemcpyHostToDevice, c.stream));
+        TN_CUDA(cudaMemcpyAsync(dt.p, target_ones, sizeof(int) * n_groups, cudaMemcpyHostToDevice, c.stream));
+      }
+      observables(c, db.as<uint8_t>(), dq.as<double>(), dp.as<double>(), n, N, n_groups ? dg.as<int>() : nullptr,
+                  n_groups, dt.as<int>(), dw.as<double>(), dpass.as<double>(), ds.as<double>());
+      std::vector<double> h(3 * (N + 1));
+      TN_CUDA(cudaMemcpyAsync(h.data(), ds.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c.stream));
+      TN_CUDA(cudaStreamSynchronize(c.stream));
+      for (int v = 0; v < N; ++v) {
+        out_z_weighted[v] = h[3 * v + 2] > 0 ? h[3 * v] / h[3 * v + 2] : NAN;
+        out_z_plain[v] = h[3 * v + 1] / (double)n;
+      }
+      *out_pass_rate = h[3 * N] / (double)n;
+      if (out_pass_rate_weighted) *out_pass_rate_weighted = h[3 * N + 2] > 0 ? h[3 * N + 1] / h[3 * N + 2] : NAN;
+    }
+    TN_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
 

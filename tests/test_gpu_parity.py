@@ -393,3 +393,83 @@ def test_w16_willow_vs_oracle_golden():
     rep = compare_samples(order_of(lat.rows), u, bits, logq, cond, ref["bits"], ref["logq"], ref["cond"])
     print("w16", rep)
     assert rep["compared"] >= (len(u) - 1) * lat.n
+
+
+# ------------------------------------------------------------------ configs 3 and 5 (topologies)
+def test_cfg5_lucj_reduced_vs_oracle():
+    """Config 5 topology (LUCJ-like 52-qubit two-register ladder, rows = rung pairs, PAPER.md:
+    147-155) with the synthetic LUCJ circuit of the oracle generator (XX+YY brickwork, CP on the
+    rungs, HF-like start) at reduced depth and bond (chi = 16, 4 + 4 layers) and chi_env = 16:
+    every conditional, ln q and bit against the oracle (R16); particle number per register
+    is conserved by every gate, so the samples lie in the HF sector."""
+    lat, st = G.config_state("cfg5a", chi=16, layers=4)
+    P = B.Prepared(st, lat.rows)
+    R = 16
+    M, _ = B.norm_envs(P, R)
+    u = S.uniforms(48, lat.n, 1006)
+    g, bits, logq, cond, flags = _run(st, lat.rows, R, u)
+    rb, rl, rc = oracle_samples(P, M, R, u, 16)
+    rep = compare_samples(order_of(lat.rows), u[:16], bits[:16], logq[:16], cond[:16], rb, rl, rc)
+    assert rep["compared"] >= 15 * lat.n
+    n_occ = G.LUCJ["cfg5a"][0]
+    in_sector = ((bits[:, 0::2].sum(axis=1) == n_occ) & (bits[:, 1::2].sum(axis=1) == n_occ)).mean()
+    print("cfg5 reduced", rep, "sector rate", in_sector)
+    assert in_sector > 0.9
+
+
+# ------------------------------------------------------------------ NEXT-1: path p, observables
+def test_path_amplitude_vs_statevector_and_oracle():
+    """tn_sample_path: exact regime -> ln|a| and arg a of every sample equal the
+    statevector amplitude; truncated (config 1 state, chi_env = 4) -> equal to the oracle's
+    path amplitude (oracle.bmps.sample(path_amplitude=True)) at R16."""
+    lat = L.square(3, 3)
+    st = S.vidal_like(lat, 2, seed=3, xi=2.0)
+    psi = SV.statevector(st)
+    u = S.uniforms(32, lat.n, 6)
+    g = TNState(st)
+    bits, logq, la, ph = g.sample_path(lat.rows, 16, u)
+    for k in range(len(u)):
+        a = psi[int("".join(map(str, bits[k])), 2)]
+        assert abs(la[k] - math.log(abs(a))) <= 1e-4 * max(1, abs(la[k]))
+        assert abs(np.exp(1j * (ph[k] - np.angle(a))) - 1) <= 1e-4
+    lat, st = G.config_state("cfg1")
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, 4)
+    u = S.uniforms(16, lat.n, 1001)
+    g = TNState(st)
+    bits, logq, la, ph = g.sample_path(lat.rows, 4, u)
+    for k in range(len(u)):
+        rb, rl, _, _, (ra, rp) = B.sample(P, M, 4, u[k], path_amplitude=True)
+        if not (rb == bits[k]).all():
+            continue  # a boundary case: the draw diverged (counted by the conditional tests)
+        assert abs(la[k] - ra) <= 1e-4 * max(1, abs(ra)), (k, la[k], ra)
+        assert abs(np.exp(1j * (ph[k] - rp)) - 1) <= 1e-4
+
+
+def test_observables_vs_oracle_metrics():
+    """tn_observables on GPU samples at finite chi_env with ln p from
+    tn_certify: importance-sampled <Z_v> equals oracle.metrics.importance_expectation on the same
+    (ln q, ln p, z_v); the sector pass rate equals the fraction of samples in the domain wall's
+    magnetisation sector; with 512 samples the importance estimate of <Z_v> lies within 5
+    standard errors of the statevector value."""
+    from oracle import metrics
+    from paper_2507_11424_b200 import observables
+    lat, st = G.config_state("cfg1")
+    psi = SV.statevector(st)
+    u = S.uniforms(512, lat.n, 41)
+    g = TNState(st)
+    bits, logq, _, _ = g.sample(lat.rows, 4, u)
+    lp, _ = g.certify(bits, logq, 16)
+    target = sum(L.domain_wall_bits(lat))
+    res = observables(bits, logq, lp, groups=[0] * lat.n, targets=[target])
+    assert abs(res["pass_rate"] - (bits.sum(axis=1) == target).mean()) < 1e-12
+    p = np.abs(psi) ** 2
+    p /= p.sum()
+    idx = np.arange(len(p))
+    for v in range(lat.n):
+        z = 1 - 2 * bits[:, v].astype(float)
+        assert abs(res["z_weighted"][v] - metrics.importance_expectation(logq, lp, z)) < 1e-9
+        assert abs(res["z_plain"][v] - z.mean()) < 1e-12
+        zv = 1 - 2 * ((idx >> (lat.n - 1 - v)) & 1)
+        exact = float((p * zv).sum())
+        assert abs(res["z_weighted"][v] - exact) < 5 * 2 / math.sqrt(len(u)) + 1e-9

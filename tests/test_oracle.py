@@ -525,3 +525,27 @@ def test_literal_order_truncated_is_normalised_and_differs():
     assert abs(est - p.sum()) < 1e-12 * p.sum()
     qc = _all_q(P, M, 2, lat.n)
     assert max(abs(ql[x] - qc[x]) for x in ql) > 1e-6
+
+
+def test_path_amplitude_is_exact_amplitude_in_exact_regime():
+    """with fits that make no truncation, p(x) is the square of the MPS-MPS
+    contraction m_{N_b-1 -> N_b} . X_{N_b} carried along the sampling path: ln|a| and arg a
+    equal the brute-force statevector amplitude of every sampled bitstring (3x3, exact R)."""
+    lat = L.square(3, 3)
+    st = S.vidal_like(lat, 2, seed=3, xi=2.0)
+    psi = SV.statevector(st)
+    P = B.Prepared(st, lat.rows)
+    M, _ = B.norm_envs(P, 16)
+    u = S.uniforms(10, lat.n, 6)
+    for k in range(len(u)):
+        bits, lq, _, _, (la, ph) = B.sample(P, M, 16, u[k], path_amplitude=True)
+        a = psi[int("".join(map(str, bits)), 2)]
+        assert abs(la - math.log(abs(a))) < 1e-9
+        assert abs(np.exp(1j * (ph - np.angle(a))) - 1) < 1e-9
+    # truncated (R = 2): the path amplitude is an approximation of <x|psi> (not exact)
+    M2, _ = B.norm_envs(P, 2)
+    errs = []
+    for k in range(len(u)):
+        bits, _, _, _, (la, _) = B.sample(P, M2, 2, u[k], path_amplitude=True)
+        errs.append(abs(la - math.log(abs(psi[int("".join(map(str, bits)), 2)]))))
+    assert max(errs) > 1e-6
