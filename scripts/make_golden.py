@@ -3,6 +3,7 @@
 
   python scripts/make_golden.py p1     # P1: Willow-105 L=15 domain-wall quench, chi=8, chi_env=32
   python scripts/make_golden.py w16    # Willow-105 Vidal-like state, chi=16, chi_env=64
+  python scripts/make_golden.py cfg3   # config 3: Eagle-127 L=20 quench, chi=16, chi_env=64
 
 Every stored value comes from the CPU oracle (oracle/bmps.py, complex128) on seeded inputs;
 nothing is read from the CUDA path. P1's state (SURVEY 8(d) "P1 (parity aux)") is the
@@ -32,17 +33,19 @@ CASES = {
     # name: (state recipe, chi, chi_env, n samples, uniform seed)
     "p1": ("quench", 8, 32, 64, 1008),
     "w16": ("vidal_like", 16, 64, 8, 1016),
+    "cfg3": ("quench", 16, 64, 24, 1003),
 }
 
 
 def state_for(name):
     recipe, chi, *_ = CASES[name]
-    lat = L.willow105()
+    cfg = {"p1": "P1", "cfg3": "cfg3"}.get(name)
+    lat = L.by_name(G.CONFIGS[cfg][0]) if cfg else L.willow105()
     if recipe == "quench":
         path = os.path.join(GOLDEN, f"{name}_state.npz")
         if os.path.exists(path):
             return lat, load_p1_state(path)
-        _, layers = G.CONFIGS["P1"][1], G.CONFIGS["P1"][3]
+        layers = G.CONFIGS[cfg][3]
         st = G.heisenberg_quench(lat, chi, layers)
         st["tensors"] = [t.astype(np.complex64).astype(np.complex128) for t in st["tensors"]]
         meta = {k: v for k, v in st["meta"].items() if np.ndim(v) == 0}

@@ -473,3 +473,21 @@ def test_observables_vs_oracle_metrics():
         zv = 1 - 2 * ((idx >> (lat.n - 1 - v)) & 1)
         exact = float((p * zv).sum())
         assert abs(res["z_weighted"][v] - exact) < 5 * 2 / math.sqrt(len(u)) + 1e-9
+
+
+def test_cfg3_eagle_quench_vs_oracle_golden():
+    """Config 3: IBM Eagle-127 heavy-hex domain-wall Heisenberg quench, L = 20,
+    chi = 16 (the oracle generator's state rounded to complex64, tests/golden/cfg3_state.npz),
+    chi_env = 64: conditionals, ln q and bits of 24 samples against the CPU oracle
+    (tests/golden/cfg3_oracle.npz, scripts/make_golden.py cfg3), at R16; U(1) pass rate."""
+    import os
+    ref = _golden("cfg3")
+    st = S.load_state(os.path.join(GOLDEN, "cfg3_state.npz"))
+    st["tensors"] = [np.asarray(t, dtype=np.complex128) for t in st["tensors"]]
+    lat = L.eagle127()
+    R = int(ref["chi_env"])
+    u = S.uniforms(len(ref["logq"]), lat.n, int(ref["uniform_seed"]))
+    g, bits, logq, cond, flags = _run(st, lat.rows, R, u)
+    rep = compare_samples(order_of(lat.rows), u, bits, logq, cond, ref["bits"], ref["logq"], ref["cond"])
+    print("cfg3", rep, "U(1) pass", (bits.sum(axis=1) == sum(L.domain_wall_bits(lat))).mean())
+    assert rep["compared"] >= (len(u) - 2) * lat.n
