@@ -1048,6 +1048,416 @@ __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
   }
 }
 
+
+// 3M operand planes: six K-major FP16 planes [z][Rrows][Krp] (Krp = padded complex K) at
+// stride pstride elements: (Xr, Xi, Xr + Xi) x (hi, lo) of the row-scaled operand (conj
+// applied first). Same gather as prep_wide_kernel (whole 32 x PK_K tile loaded first); each
+// thread then writes two consecutive k of one row as half2 into every plane.
+__global__ void __launch_bounds__(256, 4) prep3m_wide_kernel(PrepArgs a, int64_t pstride) {
+  __shared__ float2 tile[32][PK_K + 1];
+  __shared__ int64_t roff[32], koff[PK_K];
+  __shared__ float scl[32];
+  const int r0 = blockIdx.x * 32, k0 = blockIdx.y * PK_K, zz = blockIdx.z;
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  if (t >= 224) {
+    const int i = t - 224;
+    const float m = (r0 + i < a.R) ? prep_rowmax(a, zz, r0 + i) : 0.f;
+    scl[i] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
+  }
+  prep_offsets(a, roff, koff, r0, k0);
+  const float2* base = prep_base(a, zz);
+  float2 v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int rr = a.k_fast ? ty + 8 * (i & 3) : tx;
+    const int kk = a.k_fast ? (i >> 2) * 32 + tx : ty + 8 * i;
+    const int64_t ro = roff[rr], ko = koff[kk];
+    v[i] = make_float2(0.f, 0.f);
+    if (ro >= 0 && ko >= 0) v[i] = base[ro + ko];
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int rr = a.k_fast ? ty + 8 * (i & 3) : tx;
+    const int kk = a.k_fast ? (i >> 2) * 32 + tx : ty + 8 * i;
+    float2 w = v[i];
+    if (a.conj) w.y = -w.y;
+    tile[rr][kk] = w;
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)a.Rrows * a.Krp;
+  const int kp = a.Krp >> 1;  // half2 per plane row
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int item = t + 256 * it;  // (row, k pair): 32 x 64
+    const int r = item >> 6, kq = item & 63;
+    const int row = r0 + r, kc = (k0 >> 1) + kq;  // half2 index within the plane row
+    if (row >= a.Rrows || 2 * kc >= a.Krp) continue;
+    const float2 x0 = tile[r][2 * kq], x1 = tile[r][2 * kq + 1];
+    const float sc = scl[r];
+    const float re0 = x0.x * sc, im0 = x0.y * sc, re1 = x1.x * sc, im1 = x1.y * sc;
+    __half2 h, l;
+    __half2* P = reinterpret_cast<__half2*>(a.hi + zz * plane) + (int64_t)row * kp + kc;
+    split16x2(re0, re1, h, l);
+    P[0] = h;
+    P[pstride >> 1] = l;
+    split16x2(im0, im1, h, l);
+    P[2 * (pstride >> 1)] = h;
+    P[3 * (pstride >> 1)] = l;
+    split16x2(re0 + im0, re1 + im1, h, l);
+    P[4 * (pstride >> 1)] = h;
+    P[5 * (pstride >> 1)] = l;
+  }
+}
+
+// 3M planes of a K-contiguous operand (no transpose): 8 rows per CTA, each thread two
+// consecutive complex k (one 16-byte load) -> one half2 per plane.
+__global__ void __launch_bounds__(256) prep3m_kfast_kernel(PrepArgs a, int64_t pstride) {
+  __shared__ int64_t roff[PKF_ROWS];
+  __shared__ float scl[PKF_ROWS];
+  const int r0 = blockIdx.x * PKF_ROWS, zz = blockIdx.z;
+  const int t = threadIdx.x;
+  if (t < PKF_ROWS) {
+    const int r = r0 + t;
+    roff[t] = (r < a.R) ? view_off(a.vr, r) : -1;
+    const float m = (r < a.R) ? prep_rowmax(a, zz, r) : 0.f;
+    scl[t] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
+  }
+  const int kpair = blockIdx.y * PKF_PAIRS + t;  // complex k = 2 kpair, 2 kpair + 1
+  const int k = 2 * kpair;
+  const bool in_plane = k < a.Krp;
+  const bool in_k = k < a.K;
+  const int64_t ko = in_k ? view_off(a.vk, k) : 0;
+  __syncthreads();
+  if (!in_plane) return;
+  const float2* base = prep_base(a, zz);
+  const int64_t plane = (int64_t)a.Rrows * a.Krp;
+  const int kp = a.Krp >> 1;
+#pragma unroll
+  for (int j = 0; j < PKF_ROWS; ++j) {
+    const int r = r0 + j;
+    if (r >= a.Rrows) break;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (in_k && roff[j] >= 0) v = *reinterpret_cast<const float4*>(base + roff[j] + ko);
+    if (a.conj) {
+      v.y = -v.y;
+      v.w = -v.w;
+    }
+    const float sc = scl[j];
+    const float re0 = v.x * sc, im0 = v.y * sc, re1 = v.z * sc, im1 = v.w * sc;
+    __half2 h, l;
+    __half2* P = reinterpret_cast<__half2*>(a.hi + zz * plane) + (int64_t)r * kp + kpair;
+    split16x2(re0, re1, h, l);
+    P[0] = h;
+    P[pstride >> 1] = l;
+    split16x2(im0, im1, h, l);
+    P[2 * (pstride >> 1)] = h;
+    P[3 * (pstride >> 1)] = l;
+    split16x2(re0 + im0, re1 + im1, h, l);
+    P[4 * (pstride >> 1)] = h;
+    P[5 * (pstride >> 1)] = l;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// 3M (Gauss) complex GEMM on the CTA pair. C = A B is formed from three real products
+//   T1 = Ar Br,  T2 = Ai Bi,  T3 = (Ar + Ai)(Br + Bi);   Cr = T1 - T2,  Ci = T3 - T1 - T2
+// instead of the four real products of the [Re -Im; Im Re] embedding: with the FP16x3 split
+// (hi.hi + hi.lo + lo.hi per product) a complex MAC issues 9 FP16 MACs instead of 12.
+// Operands are six FP16 planes each (Xr, Xi, Xr + Xi as hi/lo, K-major [rows][K], K = the
+// complex K, exact power-of-two row / column scales as in the 4M path), streamed by TMA in
+// 32-wide K blocks (SWIZZLE_64B rows) through a 2-stage ring.
+// Accumulators: the three products need three 128-column FP32 accumulators in TMEM; the
+// fourth 128-column slot rotates so that the chunk promotion (the tensor core's FP32
+// accumulation truncates, so partial sums are moved into FP32 registers every 1024 complex
+// K) never stalls the MMA: the products restart their accumulation segments staggered by a
+// third of a chunk (product j at k-steps (j+1) C/3 + m C), so exactly one segment ends at a
+// time, segment i ending when segment i + 3 starts; segment i lives in slot i mod 4 and is
+// drained by the epilogue warps (Cr/Ci registers, signs per product) while the next ones run.
+constexpr int M3_BK = 32;                              // complex K per stage (64-byte rows)
+constexpr int M3_STAGES = 2;
+constexpr int M3_NC = 128;                             // complex columns per tile (MMA N = 128)
+constexpr int M3_APLANE = 128 * M3_BK * 2;             // 8 KB: 128 rows of one A plane (per CTA)
+constexpr int M3_BPLANE = 64 * M3_BK * 2;              // 4 KB: 64 rows of one B plane (per CTA)
+constexpr int M3_STAGE = 6 * M3_APLANE + 6 * M3_BPLANE;  // 72 KB
+constexpr int M3_SMEM = M3_STAGES * M3_STAGE + EPI_STAGE_BYTES + EPI_COLSC_BYTES + 1024 + 512;
+constexpr int M3_C = 64;                               // k-steps (16 complex K) per segment: 1024 K
+
+struct Maps12 {
+  CUtensorMap m[12];  // A planes 0..5 (Ar hi/lo, Ai hi/lo, As hi/lo), then B planes 0..5
+};
+
+__device__ __forceinline__ uint64_t smem_desc64(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((512 >> 4) & 0x3FFF) << 32;  // SBO: 8-row atoms of 64 B
+  d |= (uint64_t)1 << 46;                      // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;                      // SWIZZLE_64B
+  return d;
+}
+
+// product j starts a new accumulation segment at k-step q
+__device__ __forceinline__ bool m3_start(int j, int q) {
+  if (q == 0) return true;
+  const int off = ((j + 1) * M3_C) / 3;
+  return q >= off && ((q - off) % M3_C) == 0;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    tc_gemm3m_kernel(const __grid_constant__ Maps12 maps, TcParams p, int npm, int nn, int ntiles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + M3_STAGES * M3_STAGE);
+  uint64_t* empty = full + M3_STAGES;
+  uint64_t* slot_full = empty + M3_STAGES;
+  uint64_t* slot_empty = slot_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slot_empty + 4);
+  float2* epi_stage = reinterpret_cast<float2*>(smem + M3_STAGES * M3_STAGE + 512);
+  float* epi_colsc = reinterpret_cast<float*>(smem + M3_STAGES * M3_STAGE + 512 + EPI_STAGE_BYTES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < M3_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&slot_full[i], 1);
+      mbar_init(&slot_empty[i], 16);  // leader: 8 epilogue warps of each CTA
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < 12; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[i])));
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs)
+      const uint32_t full0 = map_to_rank(smem_u32(&full[0]), 0);
+      int i = 0;
+      for (int t = cluster; t < ntiles; t += nclusters) {
+        const PairTile tl = pair_tile(p, t, npm, nn);
+        const int mrow = (tl.mblk0 + (int)rank) * 128;
+        const int brow = tl.nblk * M3_NC + (int)rank * 64;
+        const int bz = p.b_batched ? tl.z : 0;
+        for (int q = 0; q < tl.nkb; ++q, ++i) {
+          const int kb = tl.kb0 + q;
+          const int s = i % M3_STAGES;
+          const uint32_t ph = (i / M3_STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * M3_STAGE;
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * M3_STAGE);
+          const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
+#pragma unroll
+          for (int pl = 0; pl < 6; ++pl) tma_load_3d_pair(st + pl * M3_APLANE, &maps.m[pl], kb * M3_BK, mrow, tl.z, fb);
+#pragma unroll
+          for (int pl = 0; pl < 6; ++pl)
+            tma_load_3d_pair(st + 6 * M3_APLANE + pl * M3_BPLANE, &maps.m[6 + pl], kb * M3_BK, brow, bz, fb);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // MMA issuer (leader CTA only)
+      // kind::f16 instruction descriptor: D f32, A/B f16, K-major both, N=128, M=256
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(M3_NC >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      int i = 0, seg = 0;
+      int slot_of[3] = {0, 0, 0};
+      for (int t = cluster; t < ntiles; t += nclusters) {
+        const PairTile tl = pair_tile(p, t, npm, nn);
+        for (int qb = 0; qb < tl.nkb; ++qb, ++i) {
+          const int s = i % M3_STAGES;
+          mbar_wait(&full[s], (i / M3_STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t base = smem_u32(smem + s * M3_STAGE);
+#pragma unroll
+          for (int kk = 0; kk < M3_BK / TC_UK; ++kk) {
+            const int q = qb * (M3_BK / TC_UK) + kk;
+            const uint64_t adv = (uint64_t)((kk * TC_UK * 2) >> 4);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              uint32_t acc = 1u;
+              if (m3_start(j, q)) {
+                if (q > 0) mma_commit_pair(&slot_full[slot_of[j]]);  // product j's segment is complete
+                const int sl = seg & 3;
+                mbar_wait(&slot_empty[sl], ((seg >> 2) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                slot_of[j] = sl;
+                ++seg;
+                acc = 0u;
+              }
+              const uint32_t dacc = tmem + (uint32_t)(slot_of[j] * M3_NC);
+              const uint64_t ahi = smem_desc64(base + (2 * j) * M3_APLANE) + adv;
+              const uint64_t alo = smem_desc64(base + (2 * j + 1) * M3_APLANE) + adv;
+              const uint64_t bhi = smem_desc64(base + 6 * M3_APLANE + (2 * j) * M3_BPLANE) + adv;
+              const uint64_t blo = smem_desc64(base + 6 * M3_APLANE + (2 * j + 1) * M3_BPLANE) + adv;
+              mma_f16_pair(dacc, ahi, bhi, idesc, acc);
+              mma_f16_pair(dacc, ahi, blo, idesc, 1u);
+              mma_f16_pair(dacc, alo, bhi, idesc, 1u);
+            }
+          }
+          mma_commit_pair(&empty[s]);
+        }
+        // tile end: the three live segments, in segment-index order (= start order j0, j1, j2
+        // cyclically; the latest-started product is the last)
+        const int T = tl.nkb * (M3_BK / TC_UK);
+        int last_j = 2;  // product of the most recently started segment
+        for (int q = T - 1; q >= 0; --q) {
+          bool found = false;
+          for (int j = 2; j >= 0 && !found; --j)
+            if (m3_start(j, q)) {
+              last_j = j;
+              found = true;
+            }
+          if (found) break;
+        }
+        for (int r = 1; r <= 3; ++r) mma_commit_pair(&slot_full[slot_of[(last_j + r) % 3]]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue (both CTAs): warp w drains TMEM lanes 32*(w%4).. (its rows) and complex
+    // columns [64 h, 64 h + 64) of each segment's slot, h = (w-2)/4, into Cr / Ci registers
+    const int lg = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const uint32_t slot_empty0 = map_to_rank(smem_u32(&slot_empty[0]), 0);
+    int seg = 0;
+    for (int t = cluster; t < ntiles; t += nclusters) {
+      const PairTile tl = pair_tile(p, t, npm, nn);
+      const int row = (tl.mblk0 + (int)rank) * 128 + lg * 32 + lane;
+      float acc[128];  // acc[2c] = Cr, acc[2c+1] = Ci of complex column c of this warp's half
+#pragma unroll
+      for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+      const int T = tl.nkb * (M3_BK / TC_UK);
+      for (int q = 0; q < T; ++q) {
+        for (int j = 0; j < 3; ++j) {
+          if (!m3_start(j, q)) continue;
+          const int sl = seg & 3;
+          mbar_wait(&slot_full[sl], (seg >> 2) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          // segment seg = the seg-th start event (this one): product j, drained in index order
+#pragma unroll
+          for (int cc = 0; cc < 64; cc += 16) {
+            uint32_t v[16];
+            const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(sl * M3_NC + half * 64 + cc);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int jp = j;
+#pragma unroll
+            for (int i2 = 0; i2 < 16; ++i2) {
+              const float x = __uint_as_float(v[i2]);
+              const int c = cc + i2;
+              if (jp == 0) {
+                acc[2 * c] += x;
+                acc[2 * c + 1] -= x;
+              } else if (jp == 1) {
+                acc[2 * c] -= x;
+                acc[2 * c + 1] -= x;
+              } else {
+                acc[2 * c + 1] += x;
+              }
+            }
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(slot_empty0 + (uint32_t)(sl * sizeof(uint64_t)));
+          ++seg;
+        }
+      }
+      // Coalesced output: each warp stages 32 rows x 8 complex columns in shared memory
+      // (padded rows), then writes 4 rows per store instruction (8 lanes x 8 B = 64 B each),
+      // instead of 32 scattered rows per instruction.
+      {
+        const int z = tl.z, bz = p.b_batched ? z : 0;
+        const int row0 = (tl.mblk0 + (int)rank) * 128 + lg * 32;
+        const float rs = (row < p.M) ? inv_scale(row_amax(p, z, row)) : 0.f;
+        float lmax = 0.f;
+        const float* bmx = p.bmax + (int64_t)bz * p.Np;
+        const int n0 = tl.nblk * M3_NC + half * 64;
+        float2* base;
+        int64_t ld;
+        bool acc_out = false;
+        if (p.ksplit > 1) {
+          base = p.ws + tl.split * p.ws_split + (int64_t)z * p.M * p.N;
+          ld = p.N;
+        } else {
+          const int b1 = (p.z0 + z) / p.nb2, b2 = (p.z0 + z) - b1 * p.nb2;
+          base = p.C + b1 * p.sc1 + b2 * p.sc2;
+          ld = p.cm;
+          acc_out = p.accumulate != 0;
+        }
+        float2* stg = epi_stage + (warp - 2) * 32 * (EPI_Q + 1);
+        // the tile's 64 column scales, once per warp (all lanes share the columns)
+        float* csc = epi_colsc + (warp - 2) * 64;
+        {
+          const int na = n0 + lane, nb = n0 + lane + 32;
+          csc[lane] = (na < p.N) ? inv_scale(bmx[na]) : 0.f;
+          csc[lane + 32] = (nb < p.N) ? inv_scale(bmx[nb]) : 0.f;
+        }
+        __syncwarp();
+        const int sub = lane >> 3, col = lane & 7;
+        // per-sample output bounds: one per warp when its 32 rows belong to one sample (always,
+        // unless a sample's row count is not a multiple of 32), else one atomic per element
+        const int s_lo = sample_of(p.rows_per_sample, p.z0, z, p.nb2, row0, p.amax_out_n);
+        const bool s_mixed = p.amax_out && p.ksplit == 1 &&
+                             sample_of(p.rows_per_sample, p.z0, z, p.nb2, min(row0 + 31, p.M - 1), p.amax_out_n) != s_lo;
+#pragma unroll
+        for (int q0 = 0; q0 < 64; q0 += EPI_Q) {
+#pragma unroll
+          for (int q = 0; q < EPI_Q; ++q) {
+            const float sc = rs * csc[q0 + q];
+            stg[lane * (EPI_Q + 1) + q] = make_float2(acc[2 * (q0 + q)] * sc, acc[2 * (q0 + q) + 1] * sc);
+          }
+          __syncwarp();
+          const int n = n0 + q0 + col;
+#pragma unroll 4
+          for (int r = 0; r < 32; r += 4) {
+            const int rr = r + sub, grow = row0 + rr;
+            if (grow < p.M && n < p.N) {
+              float2 val = stg[rr * (EPI_Q + 1) + col];
+              float2* dst = base + (int64_t)grow * ld + n;
+              if (acc_out) {
+                const float2 o = *dst;
+                val.x += o.x;
+                val.y += o.y;
+              }
+              *dst = val;
+              const float mv = fmaxf(fabsf(val.x), fabsf(val.y));
+              if (s_mixed)
+                atomic_max_nonneg(p.amax_out + sample_of(p.rows_per_sample, p.z0, z, p.nb2, grow, p.amax_out_n), mv);
+              lmax = fmaxf(lmax, mv);
+            }
+          }
+          __syncwarp();
+        }
+        if (p.amax_out && p.ksplit == 1 && !s_mixed) {
+          lmax = warp_max(lmax);
+          if (lane == 0) atomic_max_nonneg(p.amax_out + s_lo, lmax);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // TN_PREP_WIDE=0 selects the sub-tile prep kernel (A/B measurement only)
 bool prep_wide_on() {
   static const bool on = !(getenv("TN_PREP_WIDE") && std::atoi(getenv("TN_PREP_WIDE")) == 0);
@@ -1080,6 +1490,20 @@ CUtensorMap make_map(__half* base, int inner, int rows, int nz, int box_rows) {
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(-5, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+// 3M planes: K-major FP16 rows of M3_BK = 32 elements (64 B), SWIZZLE_64B
+CUtensorMap make_map64(__half* base, int inner, int rows, int nz, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)nz};
+  cuuint64_t strides[2] = {(cuuint64_t)inner * 2, (cuuint64_t)inner * rows * 2};
+  cuuint32_t box[3] = {(cuuint32_t)M3_BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, base, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(-5, "cuTensorMapEncodeTiled (64B) failed: " + std::to_string((int)r));
   return m;
 }
 
@@ -1141,6 +1565,7 @@ extern "C" int tn_debug_gemm_log(void) {
 namespace tn {
 
 int g_zc_max = 0;  // > 0: at most this many batch elements per A-plane chunk (tn_debug_set_zc)
+int g_m3_override = -1;  // >= 0: overrides TN_3M (tn_debug_set_3m; tests)
 
 bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per_sample) {
   if (c.gemm_mode == 1) return false;
@@ -1148,6 +1573,224 @@ bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per
   if (c.gemm_mode == 2) return true;
   double work = work_per_sample > 0 ? (double)work_per_sample : (double)M * N * K;
   return work >= kTcMinWork && N >= 32 && K >= 8;
+}
+
+// Co-resident CTA pairs of a cluster kernel (a persistent grid larger than this would run its
+// surplus clusters as a serial second wave), per device.
+template <class K>
+int coresident_pairs(K kernel, int smem, std::atomic<int>* cache, int dev) {
+  int n = cache[dev & 63].load();
+  if (n) return n;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148, 1, 1);
+  cfg.blockDim = dim3(TC_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = 2;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  if (cudaOccupancyMaxActiveClusters(&n, (void*)kernel, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 64;
+  }
+  n = std::min(n, 74);
+  cache[dev & 63].store(n);
+  if (getenv("TN_GEMM_LOG")) fprintf(stderr, "coresident CTA pairs: %d\n", n);
+  return n;
+}
+
+// The 3M (Gauss) path: six FP16 planes per operand, tc_gemm3m_kernel (see above).
+void gemm_tc3m(Ctx& c, const GemmDesc& g, int dev, cudaEvent_t ev_kernel) {
+  static std::atomic<uint64_t> attr_done{0};
+  const uint64_t dbit = 1ull << (dev & 63);
+  if (!(attr_done.load() & dbit)) {
+    TN_CUDA(cudaFuncSetAttribute(tc_gemm3m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, M3_SMEM));
+    attr_done.fetch_or(dbit);
+  }
+  const int Kp = rup(g.K, M3_BK);
+  const int Mp = rup(g.M, 2 * TC_BM);
+  const int Np = rup(g.N, M3_NC);
+  const int nbz = g.nb1 * g.nb2;
+  const bool b_batched = (g.sb1 != 0 && g.nb1 > 1) || (g.sb2 != 0 && g.nb2 > 1);
+  auto simple = [](int64_t dim, int64_t stride) {
+    View4 v;
+    v.rank = 1;
+    v.dims[0] = (int)dim;
+    v.str[0] = stride;
+    return v;
+  };
+  auto inner_unit = [](const View4& v) { return v.rank > 0 && v.str[v.rank - 1] == 1; };
+  const int rows_per_sample = g.nb1 > 1 ? 0 : (g.m_per_sample > 0 ? g.m_per_sample : g.M);
+  // ---- B planes [6][nzb][Np][Kp]
+  const int nzb = b_batched ? nbz : 1;
+  const int64_t bstride = (int64_t)nzb * Np * Kp;
+  DevBuf b3((size_t)6 * bstride * 2, c.stream);
+  DevBuf bmx((size_t)nzb * Np * sizeof(float), c.stream);
+  TN_CUDA(cudaMemsetAsync(bmx.p, 0, (size_t)nzb * Np * sizeof(float), c.stream));
+  if (g.amaxC) TN_CUDA(cudaMemsetAsync(g.amaxC, 0, sizeof(float) * std::max(1, g.amaxC_n), c.stream));
+  for (int zb0 = 0; zb0 < nzb; zb0 += 65535) {
+    const int nzc = std::min(65535, nzb - zb0);
+    PrepArgs a;
+    a.X = g.B;
+    a.vr = g.vbn.rank ? g.vbn : simple(g.N, g.bn);
+    a.vk = g.vbk.rank ? g.vbk : simple(g.K, g.bk);
+    a.conj = g.conjB;
+    a.nb2 = g.nb2;
+    a.s1 = b_batched ? g.sb1 : 0;
+    a.s2 = b_batched ? g.sb2 : 0;
+    a.z0 = zb0;
+    a.R = g.N;
+    a.K = g.K;
+    a.Rrows = Np;
+    a.Krp = Kp;
+    a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
+    a.mx = bmx.as<float>() + (int64_t)zb0 * Np;
+    a.mx_sample = nullptr;
+    a.mx_sample_n = 0;
+    a.rows_per_sample = 0;
+    a.Rp = Np;
+    a.hi = b3.as<__half>() + (int64_t)zb0 * Np * Kp;
+    a.lo = nullptr;
+    dim3 gmax(ceil_div(g.N, 32), ceil_div(g.K, PK_K), nzc);
+    rowmax_wide_kernel<<<gmax, 256, 0, c.stream>>>(a);
+    TN_LAUNCHED();
+    dim3 grid(Np / 32, ceil_div(Kp, PK_K), nzc);
+    prep3m_wide_kernel<<<grid, 256, 0, c.stream>>>(a, bstride);
+    TN_LAUNCHED();
+  }
+  // ---- split-K from per-sample shapes only; splits are whole segments (1024 complex K)
+  const int kblocks = Kp / M3_BK;
+  const int seg_blocks = M3_C * TC_UK / M3_BK;
+  const int mps = g.m_per_sample > 0 ? g.m_per_sample : g.M;
+  const int64_t tiles_ps = (int64_t)((mps + TC_BM - 1) / TC_BM) * (Np / M3_NC) * g.nb2;
+  int ksplit = 1, kbps = kblocks;
+  if (tiles_ps < 148 && kblocks >= 2 * seg_blocks) {
+    int want = (int)std::min<int64_t>(32, (2 * 148 + tiles_ps - 1) / tiles_ps);
+    int maxs = kblocks / seg_blocks;
+    ksplit = std::max(1, std::min(want, maxs));
+    kbps = ((kblocks + ksplit - 1) / ksplit + seg_blocks - 1) / seg_blocks * seg_blocks;
+    ksplit = (kblocks + kbps - 1) / kbps;
+  }
+  static const bool uniform_off = getenv("TN_ROWSCALE") && std::atoi(getenv("TN_ROWSCALE")) != 0;
+  const bool use_uniform = g.amaxA != nullptr && !uniform_off;
+  // ---- A planes [6][zc][Mp][Kp], chunked over the batch (<= ~1.5 GB of planes per chunk)
+  const int64_t per_z = (int64_t)Mp * Kp;
+  const int zc0 = (int)std::max<int64_t>(
+      1, std::min<int64_t>({(int64_t)nbz, (int64_t)(65535 / ksplit), (int64_t)(1ll << 27) / std::max<int64_t>(1, per_z)}));
+  const int zc = g_zc_max > 0 ? std::min(zc0, g_zc_max) : zc0;
+  const int64_t astride = (int64_t)zc * per_z;
+  DevBuf a3((size_t)6 * astride * 2, c.stream);
+  DevBuf amx((size_t)zc * Mp * sizeof(float), c.stream);
+  DevBuf ws;
+  const int64_t ws_split = (int64_t)zc * g.M * g.N;
+  if (ksplit > 1) ws.alloc((size_t)ksplit * ws_split * sizeof(float2), c.stream);
+  const int nclusters_max = [&] {
+    static std::atomic<int> cache[64];
+    return coresident_pairs(tc_gemm3m_kernel, M3_SMEM, cache, dev);
+  }();
+  for (int z0 = 0; z0 < nbz; z0 += zc) {
+    const int nz = std::min(zc, nbz - z0);
+    PrepArgs a;
+    a.X = g.A;
+    a.vr = g.vam.rank ? g.vam : simple(g.M, g.am);
+    a.vk = g.vak.rank ? g.vak : simple(g.K, g.ak);
+    a.conj = g.conjA;
+    a.nb2 = g.nb2;
+    a.s1 = g.sa1;
+    a.s2 = g.sa2;
+    a.z0 = z0;
+    a.R = g.M;
+    a.K = g.K;
+    a.Rrows = Mp;
+    a.Krp = Kp;
+    a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
+    a.mx = amx.as<float>();
+    a.mx_sample = use_uniform ? g.amaxA : nullptr;
+    a.mx_sample_n = std::max(1, g.amaxA_n);
+    a.rows_per_sample = rows_per_sample;
+    a.Rp = Mp;
+    a.hi = a3.as<__half>();
+    a.lo = nullptr;
+    if (!use_uniform) {
+      TN_CUDA(cudaMemsetAsync(amx.p, 0, (size_t)nz * Mp * sizeof(float), c.stream));
+      dim3 gmax(ceil_div(g.M, 32), ceil_div(g.K, PK_K), nz);
+      rowmax_wide_kernel<<<gmax, 256, 0, c.stream>>>(a);
+      TN_LAUNCHED();
+    }
+    const View4& vk = a.vk;
+    bool kfast = vk.rank > 0 && vk.str[vk.rank - 1] == 1 && vk.dims[vk.rank - 1] % 2 == 0 && g.K % 2 == 0 &&
+                 (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 && a.s1 % 2 == 0 && a.s2 % 2 == 0;
+    for (int d = 0; d < vk.rank - 1 && kfast; ++d) kfast = vk.str[d] % 2 == 0;
+    for (int d = 0; d < a.vr.rank && kfast; ++d) kfast = a.vr.str[d] % 2 == 0 || a.vr.dims[d] == 1;
+    if (kfast) {
+      dim3 grid(ceil_div(Mp, PKF_ROWS), ceil_div(Kp / 2, PKF_PAIRS), nz);
+      prep3m_kfast_kernel<<<grid, 256, 0, c.stream>>>(a, astride);
+    } else {
+      dim3 grid(Mp / 32, ceil_div(Kp, PK_K), nz);
+      prep3m_wide_kernel<<<grid, 256, 0, c.stream>>>(a, astride);
+    }
+    TN_LAUNCHED();
+    Maps12 maps;
+    for (int pl = 0; pl < 6; ++pl) {
+      maps.m[pl] = make_map64(a3.as<__half>() + pl * astride, Kp, Mp, nz, 128);
+      maps.m[6 + pl] = make_map64(b3.as<__half>() + pl * bstride + (b_batched ? (int64_t)z0 * Np * Kp : 0), Kp,
+                                  Np, b_batched ? nz : 1, 64);
+    }
+    TcParams p;
+    p.M = g.M;
+    p.N = g.N;
+    p.kblocks = kblocks;
+    p.ksplit = ksplit;
+    p.kb_per_split = kbps;
+    p.ws = ws.as<float2>();
+    p.ws_split = ws_split;
+    p.b_batched = b_batched ? 1 : 0;
+    p.amax = amx.as<float>();
+    p.bmax = bmx.as<float>() + (b_batched ? (int64_t)z0 * Np : 0);
+    p.Mp = Mp;
+    p.Np = Np;
+    p.C = g.C;
+    p.cm = g.cm;
+    p.nb2 = g.nb2;
+    p.sc1 = g.sc1;
+    p.sc2 = g.sc2;
+    p.z0 = z0;
+    p.accumulate = g.accumulate ? 1 : 0;
+    p.amax_sample = use_uniform ? g.amaxA : nullptr;
+    p.amax_sample_n = std::max(1, g.amaxA_n);
+    p.amax_out = g.amaxC;
+    p.amax_out_n = std::max(1, g.amaxC_n);
+    p.rows_per_sample = rows_per_sample;
+    if (ev_kernel && z0 == 0) cudaEventRecord(ev_kernel, c.stream);
+    {
+      ProfScope ps(P_TC_KERNEL, c.stream);
+      ++g_tc_launches;
+      const int npm = Mp / (2 * TC_BM), nn = Np / M3_NC;
+      const int ntiles = nz * ksplit * npm * nn;
+      const int nclusters = std::min(ntiles, nclusters_max);
+      tc_gemm3m_kernel<<<2 * nclusters, TC_THREADS, M3_SMEM, c.stream>>>(maps, p, npm, nn, ntiles);
+      TN_LAUNCHED();
+    }
+    if (ksplit > 1) {
+      int64_t tot = (int64_t)nz * g.M * g.N;
+      unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16);
+      splitk_reduce_kernel<<<blocks, 256, 0, c.stream>>>(p.ws, ksplit, ws_split, nz, g.M, g.N, g.C, g.cm, g.nb2,
+                                                         g.sc1, g.sc2, z0, p.accumulate, g.amaxC, p.amax_out_n,
+                                                         rows_per_sample);
+      TN_LAUNCHED();
+    }
+  }
+}
+
+// 3M path selection: CTA pairs (more than 128 rows per GEMM) and K >= 512 complex (at
+// least half a segment per tile, so the tile-boundary drain is amortised). TN_3M=0 disables
+// it (A/B measurements), TN_3M=2 forces it for every pair-kernel GEMM (tests).
+int m3_mode() {
+  static const int m = getenv("TN_3M") ? std::atoi(getenv("TN_3M")) : 1;
+  return m;
 }
 
 bool gemm_tc(Ctx& c, const GemmDesc& g) {
@@ -1191,6 +1834,11 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
   // CTA pairs (M = 256 per cluster) whenever one batch element has more than 128 rows
   static const bool pair_off = getenv("TN_TC2") && std::atoi(getenv("TN_TC2")) == 0;
   const bool pair = !pair_off && g.M > TC_BM;
+  const int mm = g_m3_override >= 0 ? g_m3_override : m3_mode();
+  if (pair && mm != 0 && (g.K >= 512 || mm == 2)) {
+    gemm_tc3m(c, g, dev, slog ? srec.b : nullptr);
+    return true;
+  }
   const int Krp = rup(2 * g.K, TC_BK);
   const int Mp = rup(g.M, pair ? 2 * TC_BM : TC_BM);
   const int Nrp = rup(2 * g.N, TC_BN);
@@ -1418,6 +2066,11 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
 
 extern "C" int tn_debug_raster(int gm) {
   return cudaMemcpyToSymbol(tn::g_raster_gm, &gm, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
+
+extern "C" int tn_debug_set_3m(int mode) {
+  tn::g_m3_override = mode;
+  return 0;
 }
 
 extern "C" int tn_debug_set_zc(int zc) {

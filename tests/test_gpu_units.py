@@ -398,3 +398,38 @@ def test_gemm_per_sample_b_chunked(zc):
     ref = np.matmul(A.astype(np.complex128), B.astype(np.complex128))
     err = np.abs(out - ref).max(axis=-1) / np.abs(ref).max(axis=-1)
     print("per-sample-B max elementwise rel err", zc, err.max()); assert err.max() <= 1e-5, err.max()
+
+
+LIB.tn_debug_set_3m.argtypes = [C.c_int]
+
+
+@pytest.mark.parametrize("case", [
+    # (la, shapeA, lb, shapeB, lout, nb, perA, perB, cA, cB)
+    ("ak", (300, 600), "kb", (600, 200), "ab", 1, False, False, False, False),       # ragged M, N, K
+    ("ak", (257, 1040), "kb", (1040, 129), "ab", 1, False, False, True, False),      # conj A, ragged
+    ("sMk", (2, 260, 530), "skN", (2, 530, 70), "sMN", 3, True, True, False, True),  # batched B, conj B
+    ("mk", (1024, 2048), "kn", (2048, 256), "mn", 2, True, False, False, False),     # folded batch, 2 segments
+    ("ak", (256, 4096), "kb", (4096, 64), "ab", 1, False, False, False, False),      # split-K (few tiles)
+])
+def test_gemm_3m_forced_vs_numpy(case):
+    """The 3M (Gauss) tensor-core path (three real products T1 = Ar Br, T2 = Ai Bi,
+    T3 = (Ar + Ai)(Br + Bi), staggered TMEM accumulation segments) forced on every pair-kernel
+    GEMM (tn_debug_set_3m(2)): element-wise against an FP64 reference (max |dC| <= 1e-5
+    max |C| per row) on ragged tiles, conjugated operands, per-sample B, folded batches,
+    several promotion segments and split-K."""
+    la, sa, lb, sb, lout, nb, perA, perB, cA, cB = case
+    rng = np.random.default_rng(17)
+    A = _rand32(rng, ((nb,) + sa) if perA else sa)
+    B = _rand32(rng, ((nb,) + sb) if perB else sb)
+    LIB.tn_debug_set_3m(2)
+    try:
+        out, ref = dcontract(A, la, B, lb, lout, nb=nb, perA=perA, perB=perB, cA=cA, cB=cB, gemm=2)
+    finally:
+        LIB.tn_debug_set_3m(-1)
+    Ad = A.astype(np.complex128).conj() if cA else A.astype(np.complex128)
+    Bd = B.astype(np.complex128).conj() if cB else B.astype(np.complex128)
+    q = "Q" if (perA or perB) else ""
+    ref = np.einsum(f"{'Q' if perA else ''}{la},{'Q' if perB else ''}{lb}->{q}{lout}", Ad, Bd)
+    err = (np.abs(out - ref).max(axis=-1) / np.abs(ref).max(axis=-1)).max()
+    print("3m", la, sa, lb, sb, "max elementwise rel err", err)
+    assert np.isfinite(out).all() and err <= 1e-5, err
