@@ -1165,7 +1165,7 @@ __global__ void __launch_bounds__(256) prep3m_kfast_kernel(PrepArgs a, int64_t p
 // (hi.hi + hi.lo + lo.hi per product) a complex MAC issues 9 FP16 MACs instead of 12.
 // Operands are six FP16 planes each (Xr, Xi, Xr + Xi as hi/lo, K-major [rows][K], K = the
 // complex K, exact power-of-two row / column scales as in the 4M path), streamed by TMA in
-// 32-wide K blocks (SWIZZLE_64B rows) through a 2-stage ring.
+// 16-wide K blocks (SWIZZLE_32B rows) through a 5-stage ring.
 // Accumulators: the three products need three 128-column FP32 accumulators in TMEM; the
 // fourth 128-column slot rotates so that the chunk promotion (the tensor core's FP32
 // accumulation truncates, so partial sums are moved into FP32 registers every 1024 complex
@@ -1173,12 +1173,12 @@ __global__ void __launch_bounds__(256) prep3m_kfast_kernel(PrepArgs a, int64_t p
 // third of a chunk (product j at k-steps (j+1) C/3 + m C), so exactly one segment ends at a
 // time, segment i ending when segment i + 3 starts; segment i lives in slot i mod 4 and is
 // drained by the epilogue warps (Cr/Ci registers, signs per product) while the next ones run.
-constexpr int M3_BK = 32;                              // complex K per stage (64-byte rows)
-constexpr int M3_STAGES = 2;
+constexpr int M3_BK = 16;                              // complex K per stage (32-byte rows)
+constexpr int M3_STAGES = 5;
 constexpr int M3_NC = 128;                             // complex columns per tile (MMA N = 128)
-constexpr int M3_APLANE = 128 * M3_BK * 2;             // 8 KB: 128 rows of one A plane (per CTA)
-constexpr int M3_BPLANE = 64 * M3_BK * 2;              // 4 KB: 64 rows of one B plane (per CTA)
-constexpr int M3_STAGE = 6 * M3_APLANE + 6 * M3_BPLANE;  // 72 KB
+constexpr int M3_APLANE = 128 * M3_BK * 2;             // 4 KB: 128 rows of one A plane (per CTA)
+constexpr int M3_BPLANE = 64 * M3_BK * 2;              // 2 KB: 64 rows of one B plane (per CTA)
+constexpr int M3_STAGE = 6 * M3_APLANE + 6 * M3_BPLANE;  // 36 KB
 constexpr int M3_SMEM = M3_STAGES * M3_STAGE + EPI_STAGE_BYTES + EPI_COLSC_BYTES + 1024 + 512;
 constexpr int M3_C = 64;                               // k-steps (16 complex K) per segment: 1024 K
 
@@ -1189,9 +1189,9 @@ struct Maps12 {
 __device__ __forceinline__ uint64_t smem_desc64(uint32_t addr) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
-  d |= (uint64_t)((512 >> 4) & 0x3FFF) << 32;  // SBO: 8-row atoms of 64 B
+  d |= (uint64_t)((256 >> 4) & 0x3FFF) << 32;  // SBO: 8-row atoms of 32 B
   d |= (uint64_t)1 << 46;                      // descriptor version (sm_100)
-  d |= (uint64_t)4 << 61;                      // SWIZZLE_64B
+  d |= (uint64_t)6 << 61;                      // SWIZZLE_32B
   return d;
 }
 
@@ -1493,7 +1493,7 @@ CUtensorMap make_map(__half* base, int inner, int rows, int nz, int box_rows) {
   return m;
 }
 
-// 3M planes: K-major FP16 rows of M3_BK = 32 elements (64 B), SWIZZLE_64B
+// 3M planes: K-major FP16 rows of M3_BK = 16 elements (32 B), SWIZZLE_32B
 CUtensorMap make_map64(__half* base, int inner, int rows, int nz, int box_rows) {
   CUtensorMap m;
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)nz};
@@ -1501,7 +1501,7 @@ CUtensorMap make_map64(__half* base, int inner, int rows, int nz, int box_rows) 
   cuuint32_t box[3] = {(cuuint32_t)M3_BK, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, base, dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(-5, "cuTensorMapEncodeTiled (64B) failed: " + std::to_string((int)r));
   return m;
@@ -1785,11 +1785,14 @@ void gemm_tc3m(Ctx& c, const GemmDesc& g, int dev, cudaEvent_t ev_kernel) {
   }
 }
 
-// 3M path selection: CTA pairs (more than 128 rows per GEMM) and K >= 512 complex (at
-// least half a segment per tile, so the tile-boundary drain is amortised). TN_3M=0 disables
-// it (A/B measurements), TN_3M=2 forces it for every pair-kernel GEMM (tests).
+// 3M path selection. OFF by default: measured on B200 (profiles/r02_ncu_gemm_3m_vs_4m.json)
+// the 3M kernel is bound by shared-memory bandwidth (l1tex 92 %, tensor pipe 42 % active vs
+// 50 % / 93 % for the 4M kernel at M=16384, N=K=4096): N = 128 per product (three
+// accumulators + a rotating slot in 512 TMEM columns) and six planes per operand make its
+// operand tiles per MMA cycle 1.5x larger, and the TMA fills share the port. TN_3M=1 enables
+// it for pair GEMMs with K >= 512 (complex), TN_3M=2 for every pair GEMM (tests).
 int m3_mode() {
-  static const int m = getenv("TN_3M") ? std::atoi(getenv("TN_3M")) : 1;
+  static const int m = getenv("TN_3M") ? std::atoi(getenv("TN_3M")) : 0;
   return m;
 }
 
