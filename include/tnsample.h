@@ -37,7 +37,7 @@ extern "C" {
 #define TN_E_ROWS (-3)    /* row order not a grid-layered line partition (R1) */
 #define TN_E_NOMEM (-4)   /* device or host allocation failed */
 #define TN_E_CUDA (-5)    /* CUDA runtime error or no device */
-#define TN_E_NCCL (-6)    /* reserved: collectives run in the Python driver (torch.distributed) */
+#define TN_E_NCCL (-6)    /* NCCL error (tn_comm_unique_id, tn_set_comm, sharded tn_prepare) */
 #define TN_E_NUMERIC (-7) /* non-finite value in the norm-environment precompute */
 
 /* Per-sample incident flags (not errors). */
@@ -71,6 +71,20 @@ int tn_load_state(const tn_graph* g, const double* const* tensors, int32_t chi, 
  * row order (used by tn_amplitude). */
 int tn_prepare(tn_state* st, const int32_t* row_ptr, const int32_t* row_vertices, int32_t n_rows,
                int32_t chi_env);
+
+/* Sharded norm-environment precompute. The double-layer
+ * fits of tn_prepare loop over chunks of their output-bond rows (the mid contraction
+ * L.M.A.conj(A) of one chunk at a time); after tn_set_comm, chunk ci is computed only by rank
+ * ci % world and broadcast from it over NCCL (NVLink), and every rank assembles the chunks in
+ * the same order as one GPU: the environments are bitwise identical on every rank and to a
+ * one-GPU tn_prepare. All ranks must call tn_prepare with the same arguments. Everything else
+ * (sampling) stays rank-local; the sample shards are the caller's (paper_2507_11424_b200.dist).
+ * tn_comm_unique_id: rank 0 creates the id (TN_COMM_ID_BYTES opaque bytes), the caller
+ * distributes it; tn_set_comm: every rank joins (blocking until all have joined) on the
+ * state's device. Errors: TN_E_ARG, TN_E_NCCL, TN_E_CUDA. */
+#define TN_COMM_ID_BYTES 128
+int tn_comm_unique_id(uint8_t* out_id);
+int tn_set_comm(tn_state* st, const uint8_t* id, int32_t rank, int32_t world);
 
 /* Draw n_samples bitstrings from q(x). uniforms[k][v] in [0,1) is
  * the random number of sample k at vertex id v: x_v = 0 iff u < P0 (R10). Outputs are
@@ -170,7 +184,9 @@ int tn_observables(const uint8_t* bits, const double* logq, const double* logp, 
  * order: 0 = compress-then-sample, R3, default; 1 = the paper's literal order, PAPER.md:
  * 289-290 -- sample row b against the uncompressed m_{b-1}.psi_b five-layer ladder, then fit
  * the projected row; its environments hold chi_env^3 chi^2 entries, meant for chi_env <=
- * chi). Changing fit_half_sweeps / init_seed / gemm invalidates cached environments.
+ * chi), "chunk_elems" (element budget of one chunk of the double-layer mid contraction in
+ * tn_prepare, 0 = default 2^30; smaller = more chunks, e.g. to spread a sharded precompute).
+ * Changing fit_half_sweeps / init_seed / gemm / chunk_elems invalidates cached environments.
  * Unknown name or value -> TN_E_ARG. */
 int tn_set_option(tn_state* st, const char* name, int64_t value);
 

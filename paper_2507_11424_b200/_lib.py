@@ -18,7 +18,7 @@ ERRORS = {-1: "TN_E_ARG", -2: "TN_E_GRAPH", -3: "TN_E_ROWS", -4: "TN_E_NOMEM", -
           -6: "TN_E_NCCL", -7: "TN_E_NUMERIC"}
 EXPORTS = ["tn_load_state", "tn_prepare", "tn_sample", "tn_sample_ex", "tn_sample_dev", "tn_sample_path",
            "tn_amplitude", "tn_log_norm", "tn_certify", "tn_observables", "tn_set_option", "tn_get_stats",
-           "tn_free_state", "tn_last_error"]
+           "tn_comm_unique_id", "tn_set_comm", "tn_free_state", "tn_last_error"]
 
 
 class TNError(RuntimeError):
@@ -52,6 +52,8 @@ def load_library(path: str = LIB_PATH):
     lib.tn_sample_path.argtypes = [P, i32p, i32p, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P]
     lib.tn_observables.argtypes = [P, P, P, C.c_int64, C.c_int32, P, C.c_int32, P, P, P, P, P]
     lib.tn_amplitude.argtypes = [P, P, C.c_int64, C.c_int32, P, P]
+    lib.tn_comm_unique_id.argtypes = [P]
+    lib.tn_set_comm.argtypes = [P, P, C.c_int32, C.c_int32]
     lib.tn_log_norm.argtypes = [P, C.c_int32, C.POINTER(C.c_double)]
     lib.tn_certify.argtypes = [P, P, P, C.c_int64, C.c_int32, C.c_double, P, C.POINTER(CertStats)]
     lib.tn_set_option.argtypes = [P, C.c_char_p, C.c_int64]
@@ -167,6 +169,11 @@ class TNState:
                                     _ptr(ph)))
         return bits, logq, la, ph
 
+    def set_comm(self, uid: bytes, rank: int, world: int):
+        """tn_set_comm: join the NCCL communicator that shares tn_prepare (NEXT-2)."""
+        buf = np.frombuffer(bytes(uid), dtype=np.uint8).copy()
+        _check(lib().tn_set_comm(self._h, _ptr(buf), int(rank), int(world)))
+
     def amplitude(self, bits, chi_env: int):
         b = np.ascontiguousarray(bits, dtype=np.uint8)
         n = b.shape[0]
@@ -220,3 +227,10 @@ def observables(bits, logq, logp, groups=None, targets=None):
     _check(lib().tn_observables(_ptr(b), _ptr(q), _ptr(lp), n, N, _ptr(g), ng, _ptr(t), _ptr(zw), _ptr(zp),
                                 C.byref(pr), C.byref(prw)))
     return {"z_weighted": zw, "z_plain": zp, "pass_rate": pr.value, "pass_rate_weighted": prw.value}
+
+
+def comm_unique_id() -> bytes:
+    """tn_comm_unique_id: a new NCCL unique id (rank 0), to be sent to the other ranks."""
+    buf = np.zeros(128, dtype=np.uint8)
+    _check(lib().tn_comm_unique_id(_ptr(buf)))
+    return buf.tobytes()

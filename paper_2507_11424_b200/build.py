@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         msg = "\n".join(f"--- {s}\n{o}" for s, o in failed)
         raise RuntimeError("nvcc failed:\n" + msg)
-    cmd = [nvcc, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-lcuda"]
+    cmd = [nvcc, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-lcuda", "-lnccl"]
     subprocess.run(cmd, check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT

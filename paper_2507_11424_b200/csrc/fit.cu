@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <cstdio>
 
+#include <nccl.h>
+
 #include "fit.h"
 #include "kernels.h"
 #include "linalg.h"
@@ -117,6 +119,69 @@ struct Ops {
     return contract(c, X2, "xbDfsur", false, A, "sUDbR", true, "xfurUR");
   }
 
+  // Double-layer chunk loops. fn(x0, x1) returns the part of chunk
+  // [x0, x1). concat: the parts are rows x0..x1-1 of a tensor of shape `shape`; else the result
+  // is the sum of the parts (shape `shape`) in chunk order. With a communicator (Ctx::comm)
+  // chunk ci is computed by rank ci % world only and broadcast from it; every rank then
+  // assembles the same bits in the same order as one GPU does (no reduction across ranks).
+  template <class Fn>
+  Tensor chunked(int nx, int step, bool concat, const std::vector<int>& shape, Fn fn) {
+    const int nch = (nx + step - 1) / step;
+    ncclComm_t comm = reinterpret_cast<ncclComm_t>(c.comm);
+    if (!comm) {  // one GPU
+      Tensor out;
+      for (int x0 = 0; x0 < nx; x0 += step) {
+        const int x1 = std::min(nx, x0 + step);
+        Tensor part = fn(x0, x1);
+        if (concat) {
+          if (nch == 1) return part;
+          if (!out.p) out = new_tensor(c, shape, false);
+          copy_rows(c, part, out, x0, 1);
+        } else {
+          if (!out.p) out = part;
+          else add_into(c, out, part, 1);
+        }
+      }
+      return out;
+    }
+    auto nccl = [](ncclResult_t r) {
+      if (r != ncclSuccess) throw Error(-6, std::string("NCCL: ") + ncclGetErrorString(r));
+    };
+    if (concat) {
+      Tensor out = new_tensor(c, shape, false);
+      const int64_t row = out.size() / shape[0];
+      for (int ci = 0; ci < nch; ++ci) {
+        const int x0 = ci * step, x1 = std::min(nx, x0 + step);
+        if (ci % c.world == c.rank) copy_rows(c, fn(x0, x1), out, x0, 1);
+      }
+      invalidate_amax(out);
+      nccl(ncclGroupStart());
+      for (int ci = 0; ci < nch; ++ci) {
+        const int x0 = ci * step, x1 = std::min(nx, x0 + step);
+        float* p = reinterpret_cast<float*>(out.p + (int64_t)x0 * row);
+        nccl(ncclBroadcast(p, p, (size_t)(x1 - x0) * row * 2, ncclFloat, ci % c.world, comm, c.stream));
+      }
+      nccl(ncclGroupEnd());
+      return out;
+    }
+    std::vector<Tensor> parts(nch);
+    for (int ci = 0; ci < nch; ++ci) {
+      const int x0 = ci * step, x1 = std::min(nx, x0 + step);
+      if (ci % c.world == c.rank) parts[ci] = fn(x0, x1);
+      else parts[ci] = new_tensor(c, shape, false);
+      invalidate_amax(parts[ci]);
+    }
+    nccl(ncclGroupStart());
+    for (int ci = 0; ci < nch; ++ci) {
+      float* p = reinterpret_cast<float*>(parts[ci].p);
+      nccl(ncclBroadcast(p, p, (size_t)parts[ci].size() * 2, ncclFloat, ci % c.world, comm, c.stream));
+    }
+    nccl(ncclGroupEnd());
+    Tensor out = parts[0];
+    for (int ci = 1; ci < nch; ++ci) add_into(c, out, parts[ci], 1);
+    return out;
+  }
+
   int chunk_rows(int j, int nx) {
     const Tensor& A = s.mats[j];
     int64_t u = A.shape[1], d = A.shape[2], l = A.shape[3], r = A.shape[4];
@@ -135,25 +200,20 @@ struct Ops {
       Tensor X = mid1(L, j);
       return contract(c, X, "xnpr", false, *o, "xpz", true, "znr");
     }
-    int nx = L.shape[0];
-    int step = chunk_rows(j, nx);
-    Tensor out;
-    for (int x0 = 0; x0 < nx; x0 += step) {
-      int x1 = std::min(nx, x0 + step);
+    const int nx = L.shape[0];
+    const int step = chunk_rows(j, nx);
+    const int f = s.tops[j].p ? s.tops[j].shape[3] : L.shape[1];
+    const int r = s.mats[j].shape[4];
+    if (!o)  // non-output column: u = U = 1, rows x of [x, f, r, R]
+      return chunked(nx, step, true, {nx, f, r, r}, [&](int x0, int x1) {
+        Tensor X = mid2(L, j, x0, x1);
+        return view(X, {X.shape[0], X.shape[1], X.shape[3], X.shape[5]});
+      });
+    return chunked(nx, step, false, {o->shape[3], f, r, r}, [&](int x0, int x1) {
       Tensor X = mid2(L, j, x0, x1);
-      if (!o) {
-        Tensor part = view(X, {X.shape[0], X.shape[1], X.shape[3], X.shape[5]});
-        if (step >= nx) return part;
-        if (!out.p) out = new_tensor(c, {nx, part.shape[1], part.shape[2], part.shape[3]}, false);
-        copy_rows(c, part, out, x0, 1);
-      } else {
-        Tensor oc = slice_rows(*o, x0, x1);
-        Tensor part = contract(c, X, "xfurUR", false, oc, "xuUz", true, "zfrR");
-        if (!out.p) out = part;
-        else add_into(c, out, part, 1);
-      }
-    }
-    return out;
+      Tensor oc = slice_rows(*o, x0, x1);
+      return contract(c, X, "xfurUR", false, oc, "xuUz", true, "zfrR");
+    });
   }
 
   // d = d<o|T>/d conj(o_j) = L . (column j) . F, contracted from the left
@@ -163,18 +223,13 @@ struct Ops {
       Tensor X = mid1(L, j);
       return contract(c, X, "xnpr", false, F, "znr", false, "xpz");
     }
-    int nx = L.shape[0];
-    int step = chunk_rows(j, nx);
-    Tensor out;
-    for (int x0 = 0; x0 < nx; x0 += step) {
-      int x1 = std::min(nx, x0 + step);
+    const int nx = L.shape[0];
+    const int step = chunk_rows(j, nx);
+    const int u = s.mats[j].shape[1];
+    return chunked(nx, step, true, {nx, u, u, F.shape[0]}, [&](int x0, int x1) {
       Tensor X = mid2(L, j, x0, x1);
-      Tensor part = contract(c, X, "xfurUR", false, F, "zfrR", false, "xuUz");
-      if (step >= nx) return part;
-      if (!out.p) out = new_tensor(c, {nx, part.shape[1], part.shape[2], part.shape[3]}, false);
-      copy_rows(c, part, out, x0, 1);
-    }
-    return out;
+      return contract(c, X, "xfurUR", false, F, "zfrR", false, "xuUz");
+    });
   }
 
   // The single-layer derivative contracted from the right (rmid1), for right-to-left
@@ -200,11 +255,11 @@ struct Ops {
       return permute(c, Y2v, "nxy", "xny");
     }
     const Tensor& A = s.mats[j];
-    int nx = o ? o->shape[0] : F.shape[0];
-    int step = chunk_rows(j, nx);
-    Tensor out;
-    for (int x0 = 0; x0 < nx; x0 += step) {
-      int x1 = std::min(nx, x0 + step);
+    const int nx = o ? o->shape[0] : F.shape[0];
+    const int step = chunk_rows(j, nx);
+    const int e = s.tops[j].p ? s.tops[j].shape[0] : F.shape[1];
+    const int l = A.shape[3];
+    return chunked(nx, step, true, {nx, e, l, l}, [&](int x0, int x1) {
       Tensor Y2;
       if (o) {
         Tensor oc = slice_rows(*o, x0, x1);
@@ -215,18 +270,10 @@ struct Ops {
         Y2 = contract(c, Fc, "xfrR", false, A, "sudar", false, "fRxUsda");
       }
       Tensor Y3 = contract(c, Y2, "fRxUsda", false, A, "sUDbR", true, "fxdaDb");
-      Tensor part;
-      if (s.tops[j].p) {
-        part = contract(c, Y3, "fxdaDb", false, s.tops[j], "edDf", false, "xeab");
-      } else {
-        Tensor Y3v = view(Y3, {Y3.shape[0], Y3.shape[1], Y3.shape[3], Y3.shape[5]});
-        part = permute(c, Y3v, "fxab", "xfab");
-      }
-      if (step >= nx) return part;
-      if (!out.p) out = new_tensor(c, {nx, part.shape[1], part.shape[2], part.shape[3]}, false);
-      copy_rows(c, part, out, x0, 1);
-    }
-    return out;
+      if (s.tops[j].p) return contract(c, Y3, "fxdaDb", false, s.tops[j], "edDf", false, "xeab");
+      Tensor Y3v = view(Y3, {Y3.shape[0], Y3.shape[1], Y3.shape[3], Y3.shape[5]});
+      return permute(c, Y3v, "fxab", "xfab");
+    });
   }
 };
 

@@ -40,6 +40,10 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int gemm_mode = 0;  // 0 auto, 1 SIMT only, 2 tcgen05 whenever legal
   int nb = 1;         // number of samples in the current batch
+  // NEXT-2: an NCCL communicator (ncclComm_t) over the ranks that share the
+  // norm-environment precompute; the double-layer fits split their chunk loops across them.
+  void* comm = nullptr;
+  int rank = 0, world = 1;
 };
 
 // Allocate a tensor: per-sample (nb copies) when per_sample, else shared.

@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/tnsample.h"
 #include "fit.h"
 #include "kernels.h"
@@ -62,6 +64,7 @@ struct tn_state {
   int order = 0;  // 0: compress-then-sample (R3); 1: the paper's literal order (NEXT-3)
   uint64_t seed = 0x2507114240ull;
   int64_t max_batch = 0;
+  int64_t chunk_elems = 0;  // double-layer chunk budget override (0 = DStrip default)
   std::map<std::string, std::unique_ptr<Layout>> layouts;
   std::string cur_key;
   int64_t last_launches = 0;
@@ -247,6 +250,7 @@ Envs& norm_envs(tn_state* st, Layout& L, int R) {
     s.dbl = true;
     s.per_sample = false;
     s.W = (int)L.rows[b].size();
+    if (st->chunk_elems > 0) s.chunk_elems = st->chunk_elems;
     place_tops(L, b, E.M[b].empty() ? nullptr : &E.M[b], 1, s);
     for (int v : L.rows[b]) {
       s.mats.push_back(L.A[v]);
@@ -725,11 +729,43 @@ int tn_load_state(const tn_graph* g, const double* const* tensors, int32_t chi, 
   });
 }
 
+int tn_comm_unique_id(uint8_t* out_id) {
+  return guarded([&] {
+    if (!out_id) throw Error(TN_E_ARG, "NULL argument");
+    static_assert(sizeof(ncclUniqueId) == TN_COMM_ID_BYTES, "NCCL unique id size");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw Error(TN_E_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out_id, &id, sizeof id);
+  });
+}
+
+int tn_set_comm(tn_state* st, const uint8_t* id, int32_t rank, int32_t world) {
+  return guarded([&] {
+    if (!st || !id) throw Error(TN_E_ARG, "NULL argument");
+    if (world < 1 || rank < 0 || rank >= world) throw Error(TN_E_ARG, "rank must be in [0, world)");
+    use_device(st);
+    if (st->ctx.comm) {
+      ncclCommDestroy(reinterpret_cast<ncclComm_t>(st->ctx.comm));
+      st->ctx.comm = nullptr;
+    }
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    ncclComm_t comm;
+    ncclResult_t r = ncclCommInitRank(&comm, world, uid, rank);
+    if (r != ncclSuccess) throw Error(TN_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    st->ctx.comm = comm;
+    st->ctx.rank = rank;
+    st->ctx.world = world;
+  });
+}
+
 int tn_free_state(tn_state* st) {
   return guarded([&] {
     if (!st) return;
     cudaSetDevice(st->device);
     cudaStreamSynchronize(st->stream);
+    if (st->ctx.comm) ncclCommDestroy(reinterpret_cast<ncclComm_t>(st->ctx.comm));
     st->layouts.clear();
     cudaStreamSynchronize(st->stream);
     cudaStreamDestroy(st->stream);
@@ -756,6 +792,9 @@ int tn_set_option(tn_state* st, const char* name, int64_t value) {
     } else if (k == "max_batch") {
       st->max_batch = value;
       return;
+    } else if (k == "chunk_elems") {
+      if (value < 0) throw Error(TN_E_ARG, "chunk_elems must be >= 0");
+      st->chunk_elems = value;
     } else {
       throw Error(TN_E_ARG, "unknown option " + k);
     }

@@ -7,8 +7,11 @@ without a data-path collective:
 
 1. ``broadcast_state``  -- the TNS (graph + complex128 tensors) is broadcast from rank 0
    (NCCL over NVLink on GPUs; gloo in the CPU tests).
-2. every rank runs ``tn_prepare`` itself (deterministic kernels with batch-independent tile
-   shapes: bitwise the same environments on every rank, no communication);
+2. ``tn_prepare`` (a1) runs on every rank; by default the ranks share it (NEXT-2): the
+   double-layer fits split their chunk loops over the ranks inside libtnsample (NCCL
+   broadcast of each chunk from its owner, assembly in the same order as one GPU, so the
+   environments are bitwise the same on every rank); without sharing every rank computes all
+   of it (deterministic kernels, no communication);
 3. rank g of G draws the global samples [floor(g n / G), floor((g+1) n / G)) -- its contiguous
    shard -- reading uniforms[k] of the global sample index k (so results do not depend on G);
 4. ``all_gather_into_tensor`` of the bits (uint8) and ln q (float64), padded to the largest
@@ -126,10 +129,23 @@ class DistSampler:
         self.sampler = sampler if sampler is not None else self._gpu_sampler
         self.gather_ms = 0.0
 
-    def prepare(self):
-        """a1 on every rank (tn_prepare); deterministic, no communication."""
-        from ._lib import TNState
+    def prepare(self, shard_precompute: bool = True, chunk_elems: int = 0):
+        """a1 (tn_prepare) on every rank. With shard_precompute and more than one rank, the
+        double-layer fits are split over the ranks (NEXT-2: chunk ci computed by rank
+        ci % world, NCCL broadcast; bitwise the same environments on every rank); else every
+        rank computes all of it (deterministic, no communication)."""
+        import torch
+        from ._lib import TNState, comm_unique_id
         self._tn = TNState(self.state)
+        if chunk_elems:
+            self._tn.set_option("chunk_elems", chunk_elems)
+        if shard_precompute and self.world > 1:
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if self.rank == 0:
+                uid = torch.frombuffer(bytearray(comm_unique_id()), dtype=torch.uint8).clone()
+            uid = uid.to(self.device)
+            self.dist.broadcast(uid, 0)
+            self._tn.set_comm(uid.cpu().numpy().tobytes(), self.rank, self.world)
         self._tn.prepare(self.rows, self.R)
         return self
 

@@ -82,3 +82,29 @@ def test_dist_sampler_nccl_world1():
         assert ds.gather_ms >= 0
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_precompute_world1_bitwise():
+    """NEXT-2: tn_prepare through the sharded chunk loops (an NCCL communicator of one rank,
+    every chunk broadcast from its owner, assembled in chunk order) gives bitwise the same
+    norm environments -- hence samples, ln q and ln <psi|psi> -- as the one-GPU path with the
+    same chunking; small chunks (option chunk_elems) make every double-layer fit span
+    several chunks."""
+    from paper_2507_11424_b200._lib import comm_unique_id
+    lat = L.by_name("willow105")
+    st = S.vidal_like(lat, 4, seed=12, xi=3.0)
+    R = 16
+    u = S.uniforms(8, lat.n, 3)
+    ref = TNState(st)
+    ref.set_option("chunk_elems", 20000)
+    rb, rl, rc, _ = ref.sample(lat.rows, R, u, want_cond=True)
+    g = TNState(st)
+    g.set_option("chunk_elems", 20000)
+    g.set_comm(comm_unique_id(), 0, 1)
+    b, lq, cd, _ = g.sample(lat.rows, R, u, want_cond=True)
+    assert (b == rb).all() and np.array_equal(lq, rl) and np.array_equal(cd, rc)
+    assert g.log_norm(R) == ref.log_norm(R)
+    # default chunking: the same samples up to the summation order of the chunk partials
+    d = TNState(st)
+    db, dl, _, _ = d.sample(lat.rows, R, u, want_cond=True)
+    assert np.allclose(dl, rl, rtol=1e-4, atol=1e-6)
