@@ -306,7 +306,8 @@ def main():
         batch = a.batch
     from tninputs import lattices as L
     lat = L.by_name(lat_name)
-    config = {"workload": a.workload, "lattice": lat_name, "n_qubits": lat.n, "chi": chi, "chi_env": R,
+    config = {"precompute": "shared by the ranks (NEXT-2, NCCL)" if world > 1 else "one GPU",
+              "workload": a.workload, "lattice": lat_name, "n_qubits": lat.n, "chi": chi, "chi_env": R,
               "samples_per_gpu_per_step": batch, "fit_half_sweeps": 2, "row_order": "lattice rows",
               "within_row_order": "paper-literal (NEXT-3)" if a.order else "compress-then-sample (R3)",
               "state": "synthetic Vidal-gauge-like TNS (dense, singular-value-weighted bonds, every bond at chi)",
@@ -361,6 +362,15 @@ def main():
     g = TNState(st)
     if a.order:
         g.set_option("order", a.order)
+    if world > 1:
+        # NEXT-2: the ranks share the norm-environment precompute (tn_set_comm: the double-layer
+        # fits' chunks split over an NCCL communicator, bitwise the same environments everywhere)
+        from paper_2507_11424_b200._lib import comm_unique_id
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        g.set_comm(uid.cpu().numpy().tobytes(), rank, world)
     t_load = time.time() - t0
     t0 = time.time()
     pre_prof = np.zeros(7)
