@@ -121,8 +121,20 @@ class Clocks:
                 "samples": len(rows)}
 
 
+STATE_KIND = "vidal"
+
+
 def make_state(lat, chi):
+    """The benchmark state (--state): 'vidal' (default: Vidal-gauge-like, bond spectra
+    ~exp(-k/8)), 'vidal_steep' (spectra ~exp(-k/2)), 'branch' (K = 11 branch superposition:
+    exactly rank-deficient boundaries, the completion paths of the orthonormalisation) --
+    the same tensor shapes with different value distributions, to show that the step time
+    does not depend on the values."""
     from tninputs import synthetic as S
+    if STATE_KIND == "vidal_steep":
+        return S.vidal_like(lat, chi, seed=STATE_SEED, xi=2.0)
+    if STATE_KIND == "branch":
+        return S.branch_superposition(lat, chi, min(11, chi), seed=STATE_SEED)
     return S.vidal_like(lat, chi, seed=STATE_SEED)
 
 
@@ -295,7 +307,10 @@ def main():
                     help="0: compress-then-sample (R3, default); 1: the paper's literal order (NEXT-3, R <= chi)")
     ap.add_argument("--cpu-budget", type=float, default=40.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--state", default="vidal", choices=["vidal", "vidal_steep", "branch"])
     a = ap.parse_args()
+    global STATE_KIND
+    STATE_KIND = a.state
     assert a.warmup >= 1 and a.steps >= 1
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -310,7 +325,10 @@ def main():
               "workload": a.workload, "lattice": lat_name, "n_qubits": lat.n, "chi": chi, "chi_env": R,
               "samples_per_gpu_per_step": batch, "fit_half_sweeps": 2, "row_order": "lattice rows",
               "within_row_order": "paper-literal (NEXT-3)" if a.order else "compress-then-sample (R3)",
-              "state": "synthetic Vidal-gauge-like TNS (dense, singular-value-weighted bonds, every bond at chi)",
+              "state": {"vidal": "synthetic Vidal-gauge-like TNS (dense, singular-value-weighted bonds ~exp(-k/8), every "
+                                 "bond at chi)",
+                        "vidal_steep": "synthetic Vidal-gauge-like TNS, bond spectra ~exp(-k/2), every bond at chi",
+                        "branch": "K = 11 branch superposition at bond chi (rank-deficient boundaries)"}[a.state],
               "l2": "L2 flushed between timed steps (256 MB write); per-step working set >> 126 MB"}
 
     if a.impl == "reference":
