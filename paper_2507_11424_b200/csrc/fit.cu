@@ -236,7 +236,8 @@ struct Ops {
   // half-sweeps: the same Z then gives the new right environment (absorb_right).
   Tensor derivative_right(const Tensor& L, int j, const Tensor& F) {
     Tensor Z = rmid1(F, j);
-    return contract(c, L, "xmy", false, Z, "zmpy", false, "xpz");
+    // Z (the large operand, produced by a tensor-core GEMM with its scale bounds) as the A side
+    return contract(c, Z, "zmpy", false, L, "xmy", false, "xpz");
   }
 
   Tensor absorb_right(const Tensor& F, int j, const Tensor* o) {
