@@ -178,6 +178,35 @@ int tn_observables(const uint8_t* bits, const double* logq, const double* logp, 
                    double* out_z_weighted, double* out_z_plain, double* out_pass_rate,
                    double* out_pass_rate_weighted);
 
+/* TNS construction on the GPU, complex FP64: the
+ * state a circuit of two-qubit gates leaves, by belief propagation and the BP-gauged simple
+ * update -- the oracle generator's algorithm (O7) on the device.
+ *   tn_su_create: product state |bits> (bits[v] in {0,1}) on the graph edges [n_edges][2]
+ *                 (every bond of dimension 1).
+ *   tn_su_bp:     BP on the norm network (identity-initialised normalised messages,
+ *                 synchronous sweeps, stop when the largest message change < tol or after
+ *                 max_sweeps; R20); *out_residual, *out_sweeps (optional).
+ *   tn_su_apply2: gate on edge e (gate: 4 x 4 complex, interleaved (re, im), row-major, index
+ *                 2 x_u + x_v with u < v the edge's vertices) with the current BP messages as
+ *                 the gauge: sqrt-message gauging (eigen-based, relative cutoff 1e-12),
+ *                 orthonormal reduction of both sites, SVD, keep min(chi, #{sigma^2 / sum >
+ *                 cutoff}) >= 1 values, *out_eps = discarded weight (Eq. 1), sqrt(sigma)
+ *                 split, ungauging, normalised tensors, both messages on e := diag(sigma_kept)
+ *                 normalised. Run tn_su_bp before each layer of non-overlapping gates.
+ *   tn_su_bond_dims: [n_edges] current bond dimensions.
+ *   tn_su_export: tensors[v] (caller-allocated host complex128, C order (2, d_e1, d_e2, ...),
+ *                 e1 < e2 < ... incident edge ids): the tn_load_state layout.
+ *   tn_su_last_error: message of the last failing tn_su_* call on this thread.
+ * Errors: TN_E_ARG, TN_E_GRAPH, TN_E_CUDA. */
+typedef struct tn_su tn_su;
+int tn_su_create(int32_t n_vertices, int32_t n_edges, const int32_t* edges, const uint8_t* bits, tn_su** out);
+int tn_su_bp(tn_su* s, double tol, int32_t max_sweeps, double* out_residual, int32_t* out_sweeps);
+int tn_su_apply2(tn_su* s, int32_t edge, const double* gate, int32_t chi, double cutoff, double* out_eps);
+int tn_su_bond_dims(tn_su* s, int32_t* out);
+int tn_su_export(tn_su* s, double* const* tensors);
+int tn_su_free(tn_su* s);
+const char* tn_su_last_error(void);
+
 /* Options (SURVEY 5 "Config / flags"): "fit_half_sweeps" (nh, default 2, R5), "init_seed"
  * (default 0x2507114240, R4), "gemm" (0 = auto, 1 = force SIMT FP32, 2 = force tcgen05
  * FP16x3), "max_batch" (0 = auto from free device memory), "order" (within-row sampling

@@ -18,7 +18,8 @@ ERRORS = {-1: "TN_E_ARG", -2: "TN_E_GRAPH", -3: "TN_E_ROWS", -4: "TN_E_NOMEM", -
           -6: "TN_E_NCCL", -7: "TN_E_NUMERIC"}
 EXPORTS = ["tn_load_state", "tn_prepare", "tn_sample", "tn_sample_ex", "tn_sample_dev", "tn_sample_path",
            "tn_amplitude", "tn_log_norm", "tn_certify", "tn_observables", "tn_set_option", "tn_get_stats",
-           "tn_comm_unique_id", "tn_set_comm", "tn_free_state", "tn_last_error"]
+           "tn_comm_unique_id", "tn_set_comm", "tn_free_state", "tn_last_error", "tn_su_create", "tn_su_bp",
+           "tn_su_apply2", "tn_su_bond_dims", "tn_su_export", "tn_su_free", "tn_su_last_error"]
 
 
 class TNError(RuntimeError):
@@ -60,8 +61,15 @@ def load_library(path: str = LIB_PATH):
     lib.tn_get_stats.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
     lib.tn_free_state.argtypes = [P]
     lib.tn_last_error.restype = C.c_char_p
+    lib.tn_su_create.argtypes = [C.c_int32, C.c_int32, P, P, C.POINTER(P)]
+    lib.tn_su_bp.argtypes = [P, C.c_double, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int32)]
+    lib.tn_su_apply2.argtypes = [P, C.c_int32, P, C.c_int32, C.c_double, C.POINTER(C.c_double)]
+    lib.tn_su_bond_dims.argtypes = [P, P]
+    lib.tn_su_export.argtypes = [P, P]
+    lib.tn_su_free.argtypes = [P]
+    lib.tn_su_last_error.restype = C.c_char_p
     for name in EXPORTS:
-        if name != "tn_last_error":
+        if name not in ("tn_last_error", "tn_su_last_error"):
             getattr(lib, name).restype = C.c_int
     return lib
 
