@@ -122,6 +122,7 @@ class Clocks:
 
 
 STATE_KIND = "vidal"
+QUENCH_LAYERS = 15
 
 
 def make_state(lat, chi):
@@ -131,6 +132,16 @@ def make_state(lat, chi):
     the same tensor shapes with different value distributions, to show that the step time
     does not depend on the values."""
     from tninputs import synthetic as S
+    if STATE_KIND == "quench":
+        # the paper's workload itself: the domain-wall Heisenberg quench (config 4b: L = 15 Trotter
+        # layers, dt = 0.1), built on the GPU by libtnsample's BP-gauged simple update (NEXT-4)
+        from paper_2507_11424_b200 import construct
+        from tninputs import lattices as L
+        t0 = time.time()
+        st = construct.heisenberg_quench(lat, L.domain_wall_bits(lat), chi, QUENCH_LAYERS)
+        log(f"quench state built on the GPU in {time.time() - t0:.1f} s: fidelity {st['meta']['fidelity']:.4f}, "
+            f"max bond {int(max(st['bond_dims']))}, BP residual max {st['meta']['bp_residual_max']:.2e}")
+        return st
     if STATE_KIND == "vidal_steep":
         return S.vidal_like(lat, chi, seed=STATE_SEED, xi=2.0)
     if STATE_KIND == "branch":
@@ -307,10 +318,14 @@ def main():
                     help="0: compress-then-sample (R3, default); 1: the paper's literal order (NEXT-3, R <= chi)")
     ap.add_argument("--cpu-budget", type=float, default=40.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--state", default="vidal", choices=["vidal", "vidal_steep", "branch"])
+    ap.add_argument("--state", default="vidal", choices=["vidal", "vidal_steep", "branch", "quench"])
+    ap.add_argument("--layers", type=int, default=15, help="Trotter layers of --state quench")
     a = ap.parse_args()
-    global STATE_KIND
+    global STATE_KIND, QUENCH_LAYERS
     STATE_KIND = a.state
+    QUENCH_LAYERS = a.layers
+    if a.impl == "reference" and a.state == "quench":
+        STATE_KIND = "vidal"  # the oracle's row timing depends on the shapes only (same shapes)
     assert a.warmup >= 1 and a.steps >= 1
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -328,7 +343,9 @@ def main():
               "state": {"vidal": "synthetic Vidal-gauge-like TNS (dense, singular-value-weighted bonds ~exp(-k/8), every "
                                  "bond at chi)",
                         "vidal_steep": "synthetic Vidal-gauge-like TNS, bond spectra ~exp(-k/2), every bond at chi",
-                        "branch": "K = 11 branch superposition at bond chi (rank-deficient boundaries)"}[a.state],
+                        "branch": "K = 11 branch superposition at bond chi (rank-deficient boundaries)",
+                        "quench": f"domain-wall Heisenberg quench, {a.layers} Trotter layers, dt = 0.1, built on the "
+                                  f"GPU by BP-gauged simple update (NEXT-4)"}[a.state],
               "l2": "L2 flushed between timed steps (256 MB write); per-step working set >> 126 MB"}
 
     if a.impl == "reference":
