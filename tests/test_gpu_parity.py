@@ -491,3 +491,63 @@ def test_cfg3_eagle_quench_vs_oracle_golden():
     rep = compare_samples(order_of(lat.rows), u, bits, logq, cond, ref["bits"], ref["logq"], ref["cond"])
     print("cfg3", rep, "U(1) pass", (bits.sum(axis=1) == sum(L.domain_wall_bits(lat))).mean())
     assert rep["compared"] >= (len(u) - 2) * lat.n
+
+
+def test_cfg5_lucj_full_shapes_exact():
+    """Config 5 at its full shapes (LUCJ-like 52-qubit two-register ladder, chi = 64,
+    chi_env = 256, rows = rung pairs): K = 16 branches keep every single-layer boundary at rank
+    <= 16 and every double-layer boundary at rank <= 256 = chi_env, so the method is exact
+     and every conditional and ln q must equal the closed form of the branch sum."""
+    from tests.test_oracle import closed_form_conditionals
+    lat = L.by_name("lucj52")
+    st = S.branch_superposition(lat, 64, 16, seed=31)
+    u = S.uniforms(4, lat.n, 37)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 256, u)
+    order = order_of(lat.rows)
+    assert (flags == 0).all()
+    for k in range(len(u)):
+        ref = closed_form_conditionals(st["meta"]["phis"], order, bits[k])
+        for v, r in zip(order, ref):
+            assert abs(cond[k, v] - r) <= 1e-4 * r + (1e-6 if r < 1e-2 else 0), (k, v, cond[k, v], r)
+        assert abs(logq[k] - sum(math.log(r) for r in ref)) <= 1e-4 * max(1, abs(logq[k]))
+
+
+# ------------------------------------------------------------------ NEXT-3: chip-row partition
+def _chip(lat, st):
+    return S.split_two_edge_vertices(st, L.chip_rows(lat), [c[0] for c in lat.coords])
+
+
+def test_chip_row_partition_willow_exact_closed_form():
+    """NEXT-3: the Willow-105 chip-row ("diagonal") partition -- 15 rows of 7
+    qubits, two up and two down edges per interior qubit -- through the vertex split, on the GPU:
+    a K = 3 branch superposition at chi = 4 (split bonds chi^2 = 16, chi_env = 32 >= every
+    boundary rank) gives the closed-form conditionals of every qubit; virtual vertices draw 0."""
+    from tests.test_oracle import closed_form_conditionals
+    lat = L.willow105()
+    st = S.branch_superposition(lat, 4, 3, seed=5)
+    st2, rows2, nq = _chip(lat, st)
+    u = S.uniforms(6, st2["n"], 19)
+    g, bits, logq, cond, flags = _run(st2, rows2, 32, u)
+    order = [v for r in rows2 for v in r if v < nq]
+    assert (bits[:, nq:] == 0).all()
+    for k in range(len(u)):
+        ref = closed_form_conditionals(st["meta"]["phis"], order, bits[k, :nq])
+        for v, r in zip(order, ref):
+            assert abs(cond[k, v] - r) <= 1e-4 * r + (1e-6 if r < 1e-2 else 0), (k, v, cond[k, v], r)
+        assert abs(logq[k] - sum(math.log(r) for r in ref)) <= 1e-4 * max(1, abs(logq[k]))
+
+
+def test_chip_row_partition_vs_oracle_truncated():
+    """NEXT-3 at finite chi_env: the chip-row partition of a Willow-105 quench state (chi = 2,
+    3 layers) sampled at chi_env = 8 on the GPU against the oracle (R16), all conditionals."""
+    lat = L.willow105()
+    st = G.heisenberg_quench(lat, chi=2, layers=3)
+    st2, rows2, nq = _chip(lat, st)
+    P = B.Prepared(st2, rows2)
+    M, _ = B.norm_envs(P, 8)
+    u = S.uniforms(8, st2["n"], 23)
+    g, bits, logq, cond, flags = _run(st2, rows2, 8, u)
+    rb, rl, rc = oracle_samples(P, M, 8, u)
+    rep = compare_samples([v for r in rows2 for v in r], u, bits, logq, cond, rb, rl, rc)
+    print("chip rows", rep)
+    assert rep["compared"] > 0

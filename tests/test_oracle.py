@@ -549,3 +549,55 @@ def test_path_amplitude_is_exact_amplitude_in_exact_regime():
         bits, _, _, _, (la, _) = B.sample(P, M2, 2, u[k], path_amplitude=True)
         errs.append(abs(la - math.log(abs(psi[int("".join(map(str, bits)), 2)]))))
     assert max(errs) > 1e-6
+
+
+# ---------------------------------------------------------------- NEXT-3: chip-row partition
+def _chip_split(lat, st):
+    rows = L.chip_rows(lat)
+    return S.split_two_edge_vertices(st, rows, [c[0] for c in lat.coords])
+
+
+def test_chip_row_partition_exact_regime_is_statevector():
+    """The chip-row ("diagonal") partition of a rotated square patch, every interior
+    vertex with two up and two down edges, through the vertex split (pure re-indexing,
+    tninputs.synthetic.split_two_edge_vertices): exact regime -> the statevector conditionals
+    and ln p of the qubits; the virtual vertices always draw 0 with conditional 1."""
+    lat = L.rotated_patch(5, 5)
+    st = S.vidal_like(lat, 2, seed=4, xi=2.0)
+    st2, rows2, nq = _chip_split(lat, st)
+    assert max(len([e for e in range(len(lat.edges)) if v in lat.edges[e]]) for v in range(lat.n)) == 4
+    psi = SV.statevector(st)
+    Z = np.vdot(psi, psi).real
+    P = B.Prepared(st2, rows2)
+    M, _ = B.norm_envs(P, 64)
+    u = S.uniforms(6, st2["n"], 3)
+    order = [v for r in rows2 for v in r if v < nq]
+    for k in range(len(u)):
+        bits, lq, cond, _ = B.sample(P, M, 64, u[k])
+        assert (bits[nq:] == 0).all() and np.allclose(cond[nq:], 1.0)
+        ref = SV.conditionals(psi, nq, order, bits[:nq])
+        assert np.allclose([cond[v] for v in order], ref, atol=1e-10)
+        assert abs(lq - math.log(abs(psi[int("".join(map(str, bits[:nq])), 2)]) ** 2 / Z)) < 1e-9
+
+
+def test_chip_row_partition_truncated_is_normalised():
+    """At finite R the chip-row sampler still defines a distribution: sum_x q(x) = 1 over all
+    qubit bitstrings (virtual vertices forced to 0), and it differs from p (truncation is real)."""
+    lat = L.rotated_patch(4, 4)
+    st = S.vidal_like(lat, 3, seed=6, xi=3.0)
+    st2, rows2, nq = _chip_split(lat, st)
+    P = B.Prepared(st2, rows2)
+    M, _ = B.norm_envs(P, 2)
+    psi = SV.statevector(st)
+    p = np.abs(psi) ** 2
+    p /= p.sum()
+    tot, diff = 0.0, 0.0
+    for x in itertools.product([0, 1], repeat=nq):
+        forced = np.zeros(st2["n"], dtype=np.uint8)
+        forced[:nq] = x
+        _, lq, _, _ = B.sample(P, M, 2, np.zeros(st2["n"]), forced=forced)
+        q = math.exp(lq)
+        tot += q
+        diff = max(diff, abs(q - p[int("".join(map(str, x)), 2)]))
+    assert abs(tot - 1) < 1e-10
+    assert diff > 1e-6

@@ -162,6 +162,30 @@ def willow105() -> Lattice:
     return lat
 
 
+def rotated_patch(nx: int, ny: int) -> Lattice:
+    """A small Willow-like rotated square patch: chip points (x, y), 0 <= x < nx, 0 <= y < ny,
+    x + y even, diagonal couplings (the willow105 construction on a smaller chip; exact-regime
+    tests of the chip-row partition)."""
+    pts, coords = [], {}
+    for x in range(nx):
+        for y in range(ny):
+            if (x + y) % 2 == 0:
+                p = ((x - y) // 2 + ny // 2, (x + y) // 2)
+                pts.append(p)
+                coords[p] = (x, y)
+    return _from_points(f"rotated{nx}x{ny}", pts, coords)
+
+
+def chip_rows(lat: Lattice) -> list:
+    """The chip-row ("diagonal") partition of a rotated square lattice: rows = chip
+    rows y (display coordinates), vertices by x. Every interior vertex has two up and two down
+    edges and no edge inside its row (NEXT-3); see tninputs.synthetic.split_two_edge_vertices."""
+    rows = {}
+    for v, (x, y) in enumerate(lat.coords):
+        rows.setdefault(y, []).append(v)
+    return [sorted(rows[y], key=lambda v: lat.coords[v][0]) for y in sorted(rows)]
+
+
 def eagle127() -> Lattice:
     """IBM Eagle heavy-hex in grid coordinates (config 3).
 

@@ -184,3 +184,69 @@ def relabel(st: dict, rows: list, perm: list):
     out["bond_dims"] = np.asarray(new_bd, dtype=np.int32)
     out["tensors"] = [np.ascontiguousarray(t) for t in tensors]
     return out, new_rows
+
+
+def split_two_edge_vertices(st: dict, rows: list, xcoord) -> tuple:
+    """Rewrite a TNS so that a partition whose vertices have two up or two down edges (the
+    chip-row / "diagonal" partition of the Willow layout, NEXT-3) becomes a
+    line partition with at most one up and one down edge per vertex (R1). Pure re-indexing, no
+    arithmetic of the method: a vertex v with two up or two down edges is replaced by
+      L_v[s, left edges..., k] = delta(s, 0) delta(k, (left edges))   (no qubit: s = 1 slice zero)
+      R_v[s, right edges..., k] = A_v[s, all edges]                   (the qubit, keeps id v)
+    joined by a new edge k of dimension prod(left edge dims); 'left' edges are those whose other
+    end has a smaller xcoord. In the row, v becomes (L_v, v). The boundary between two rows then has
+    one site per crossing edge, as in the paper's diagonal contraction. L_v's drawn bit is always
+    0 with conditional 1 (its s = 1 slice vanishes), so q(x) and the qubits' bits are unchanged.
+
+    Returns (state, rows, n_qubits): vertex ids < n_qubits are the original qubits."""
+    n = st["n"]
+    edges = [tuple(int(a) for a in e) for e in np.asarray(st["edges"]).reshape(-1, 2).tolist()]
+    bd = [int(d) for d in st["bond_dims"]]
+    row_of = {v: b for b, r in enumerate(rows) for v in r}
+    inc = incident_edges(n, edges)
+    new_edges, new_bd = list(edges), list(bd)
+    tensors = [np.asarray(t) for t in st["tensors"]]
+    new_tensors = list(tensors)
+    new_rows = [list(r) for r in rows]
+    next_id = n
+    for v in range(n):
+        b = row_of[v]
+        ups = [e for e in inc[v] if row_of[edges[e][0] + edges[e][1] - v] == b - 1]
+        downs = [e for e in inc[v] if row_of[edges[e][0] + edges[e][1] - v] == b + 1]
+        if len(ups) < 2 and len(downs) < 2:
+            continue
+        assert all(row_of[edges[e][0] + edges[e][1] - v] != b for e in inc[v]), "intra-row edge at a split vertex"
+        left = [e for e in inc[v] if xcoord[edges[e][0] + edges[e][1] - v] < xcoord[v]]
+        right = [e for e in inc[v] if e not in left]
+        lv = next_id
+        next_id += 1
+        ke = len(new_edges)
+        kdim = int(np.prod([bd[e] for e in left])) if left else 1
+        new_edges.append((lv, v))
+        new_bd.append(kdim)
+        for e in left:  # the left edges now end at L_v
+            u = edges[e][0] + edges[e][1] - v
+            new_edges[e] = (u, lv)
+        # L_v: axes (s, left edges in id order, k)
+        lt = np.zeros((2,) + tuple(bd[e] for e in left) + (kdim,), dtype=np.complex128)
+        lt[0] = np.eye(kdim, dtype=np.complex128).reshape(tuple(bd[e] for e in left) + (kdim,))
+        # R_v: A_v with the left legs fused into k, axes (s, right edges in id order, k)
+        a = tensors[v]
+        pos = {e: 1 + i for i, e in enumerate(inc[v])}
+        perm = [0] + [pos[e] for e in right] + [pos[e] for e in left]
+        rt = np.transpose(a, perm).reshape((2,) + tuple(bd[e] for e in right) + (kdim,))
+        new_tensors[v] = np.ascontiguousarray(rt)
+        new_tensors.append(np.ascontiguousarray(lt))
+        r = new_rows[b]
+        r.insert(r.index(v), lv)
+    # relabel edges so that (u, v) has u < v; tensors keep legs in increasing edge id, which
+    # holds because the new edge k has the largest id at both of its ends
+    out_edges = [(min(u, w), max(u, w)) for (u, w) in new_edges]
+    out = dict(st)
+    out["n"] = next_id
+    out["edges"] = np.asarray(out_edges, dtype=np.int32).reshape(-1, 2)
+    out["bond_dims"] = np.asarray(new_bd, dtype=np.int32)
+    out["chi"] = int(max([int(st["chi"])] + new_bd))
+    out["tensors"] = new_tensors
+    out["meta"] = dict(st.get("meta", {}), split_from=n)
+    return out, new_rows, n
