@@ -306,6 +306,19 @@ def oracle_rate(st, lat, R, budget_s, seed=7, workload=None):
     return OracleTimer(st, lat, R, budget_s, seed, workload).measure()
 
 
+def apply_partition(st, lat, partition):
+    """--partition chip: the chip-row partition through the exact vertex split (NEXT-3); the
+    returned lattice stand-in carries the split network's rows and vertex count."""
+    if partition != "chip":
+        return st, lat
+    from types import SimpleNamespace
+
+    from tninputs import lattices as L
+    from tninputs import synthetic as S
+    st2, rows2, _ = S.split_two_edge_vertices(st, L.chip_rows(lat), [c[0] for c in lat.coords])
+    return st2, SimpleNamespace(rows=rows2, n=st2["n"], name=lat.name + "_chiprows", edges=st2["edges"].tolist())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -320,6 +333,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--state", default="vidal", choices=["vidal", "vidal_steep", "branch", "quench"])
     ap.add_argument("--layers", type=int, default=15, help="Trotter layers of --state quench")
+    ap.add_argument("--partition", default="rows", choices=["rows", "chip"],
+                    help="rows: lattice rows (the paper's column-wise partition, default); chip: the chip-row "
+                         "('diagonal', P:256-260) partition of Willow through the vertex split (NEXT-3)")
     a = ap.parse_args()
     global STATE_KIND, QUENCH_LAYERS
     STATE_KIND = a.state
@@ -340,6 +356,7 @@ def main():
               "workload": a.workload, "lattice": lat_name, "n_qubits": lat.n, "chi": chi, "chi_env": R,
               "samples_per_gpu_per_step": batch, "fit_half_sweeps": 2, "row_order": "lattice rows",
               "within_row_order": "paper-literal (NEXT-3)" if a.order else "compress-then-sample (R3)",
+              "partition": "chip rows via vertex split (NEXT-3)" if a.partition == "chip" else "lattice rows",
               "state": {"vidal": "synthetic Vidal-gauge-like TNS (dense, singular-value-weighted bonds ~exp(-k/8), every "
                                  "bond at chi)",
                         "vidal_steep": "synthetic Vidal-gauge-like TNS, bond spectra ~exp(-k/2), every bond at chi",
@@ -352,11 +369,12 @@ def main():
         if rank != 0:
             return
         st = make_state(lat, chi)
+        st, lat = apply_partition(st, lat, a.partition)
         # rows' cost shares: complex MACs of the oracle's own contractions, counted by a
         # shape-only dry run of oracle.bmps.sample (oracle_row_cmacs)
         # each step a bounded sample; the whole run stays within ~4 minutes after setup
         timer = OracleTimer(st, lat, R, budget_s=min(a.cpu_budget, 240.0 / (a.warmup + a.steps)),
-                            workload=a.workload)
+                            workload=a.workload + ("_chip" if a.partition == "chip" else ""))
         vals, secs = [], []
         for i in range(a.warmup + a.steps):
             cb = timer.measure()
@@ -394,6 +412,7 @@ def main():
     st = make_state(lat, chi) if rank == 0 else None
     if world > 1:
         st = broadcast_state(st, dist, dev)  # NCCL broadcast of the TNS from rank 0
+    st, lat = apply_partition(st, lat, a.partition)
     g = TNState(st)
     if a.order:
         g.set_option("order", a.order)
@@ -592,7 +611,7 @@ def main():
            "samples_per_s_incl_precompute_1e5": 1e5 / (t_pre + 1e5 / value) if value > 0 else None}
     if world == 1 and not a.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = oracle_rate(st, lat, R, budget_s=a.cpu_budget, workload=a.workload)
+            out["cpu_baseline"] = oracle_rate(st, lat, R, budget_s=a.cpu_budget, workload=a.workload + ("_chip" if a.partition == "chip" else ""))
         except Exception as e:  # pragma: no cover
             out["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "oracle",
                                    "sample": f"failed: {e}"}
