@@ -47,7 +47,14 @@ constexpr int B_TILE = TC_BN * TC_BK * 2;               // 32 KB
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;    // 96 KB
 constexpr int SMEM_BYTES = TC_STAGES * STAGE_BYTES + 1024 + 256;
 constexpr uint32_t TMEM_COLS = 512;   // two 128x256 FP32 accumulators (ping-pong over K chunks)
-constexpr int TC_KC = 16;             // k-blocks (16 x 64 real K) per promoted chunk
+constexpr int TC_KC = 16;             // split-K granularity in k-blocks (16 x 64 real K)
+// A is scaled per (row, block of SB_K complex K): one exact power of two per row and block puts
+// the block's largest |component| in [1/2, 1), so every element keeps the FP16x3 split's 22
+// significant bits relative to its own block instead of to the whole row (or sample). The
+// tensor core accumulates one block per TMEM chunk; the epilogue promotes the chunk into FP32
+// registers multiplied by the block's 1/s (FFMA), so scale blocks = promotion chunks.
+constexpr int SB_KB = 4;              // k-blocks per scale block / promoted chunk
+constexpr int SB_K = SB_KB * TC_BK / 2;  // 128 complex K
 constexpr int TC_THREADS = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 
 struct TcParams {
@@ -73,6 +80,9 @@ struct TcParams {
   int amax_out_n;             // its count
   int rows_per_sample;        // > 0: sample of row m = m / rows_per_sample (batch folded into M);
                               // 0: sample = (z0 + z) / nb2 (outer batch index)
+  const float* ascale;        // 4M kernels: [z][nsb][Mp] 1/s of A's (row, scale block) exponents
+  const float* bscale;        // 4M kernels: [zb][nsb][Np] 1/s of B's (column, scale block)
+  int nsb;                    // scale blocks (SB_KB k-blocks = SB_K complex K each) along K
 };
 
 // Sample of an M-side row (A's rows and C's rows share the mapping), for bounds of count n.
@@ -192,7 +202,6 @@ __device__ __forceinline__ void amax_out_rows(const TcParams& p, int z, int row,
 // Grouped rasterisation: linear tile id -> (m, n), groups of RASTER_GM m-tiles swept with m
 // fastest, so a wave of CTAs shares a few A strips and B strips in L2 instead of streaming
 // one operand strip per CTA from HBM (a full-K strip is 4-8 MB of FP16 planes).
-__device__ int g_kc = TC_KC;  // k-blocks per promoted chunk in the pair kernel; tn_debug_kc (experiments)
 __device__ int g_raster_gm = 16;  // group height in pair-tiles (4: +2%, 32: +4% step time); tn_debug_raster
 __device__ __forceinline__ void raster(int lin, int nm, int nn, int& m, int& n) {
   const int GM = g_raster_gm;
@@ -267,7 +276,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
       for (int i = 0; i < nkb; ++i) {
-        const int c = i / TC_KC, buf = c & 1, kin = i - c * TC_KC;
+        const int c = i / SB_KB, buf = c & 1, kin = i - c * SB_KB;
         if (kin == 0) {  // chunk c accumulates into TMEM buffer c&1 once the epilogue drained it
           mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -288,7 +297,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mma_f16(dacc, alo + adv, bhi + adv, idesc, 1u);
         }
         mma_commit(&empty[s]);
-        if (kin == TC_KC - 1 || i == nkb - 1) mma_commit(&acc_full[buf]);
+        if (kin == SB_KB - 1 || i == nkb - 1) mma_commit(&acc_full[buf]);
       }
     }
     __syncwarp();
@@ -302,9 +311,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float acc[128];
 #pragma unroll
     for (int i = 0; i < 128; ++i) acc[i] = 0.f;
-    const int nchunks = (nkb + TC_KC - 1) / TC_KC;
+    const int nchunks = (nkb + SB_KB - 1) / SB_KB;
+    const float* ascr = p.ascale + ((int64_t)z * p.nsb + kb0 / SB_KB) * p.Mp + row;  // row < Mp
+    const float* bscr = p.bscale + ((int64_t)bz * p.nsb + kb0 / SB_KB) * p.Np + ((nblk * TC_BN + half * 128) >> 1);
     for (int c = 0; c < nchunks; ++c) {
       const int buf = c & 1;
+      const float f = ascr[(int64_t)c * p.Mp];  // 1/s of this row's scale block
+      const float* fb = bscr + (int64_t)c * p.Np;  // 1/s of the block's 64 columns (< Np)
       mbar_wait(&acc_full[buf], (c >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
@@ -318,16 +331,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[cc + i] += __uint_as_float(v[i]);
+        for (int i = 0; i < 16; i += 2) {
+          const float g = f * __ldg(fb + ((cc + i) >> 1));
+          acc[cc + i] = fmaf(__uint_as_float(v[i]), g, acc[cc + i]);
+          acc[cc + i + 1] = fmaf(__uint_as_float(v[i + 1]), g, acc[cc + i + 1]);
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
     float lmax = 0.f;
-    if (row < p.M) {
-      const float rs = inv_scale(row_amax(p, z, row));
-      const float* bmx = p.bmax + (int64_t)bz * p.Np;
+    if (row < p.M) {  // (A's and B's scales were applied per block during the promotion)
       const int n0 = (nblk * TC_BN + half * 128) >> 1;
       if (p.ksplit > 1) {  // partial sum of this K split -> workspace
         float2* W = p.ws + split * p.ws_split + ((int64_t)z * p.M + row) * p.N;
@@ -335,8 +350,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int q = 0; q < 64; ++q) {
           const int n = n0 + q;
           if (n < p.N) {
-            const float sc = rs * inv_scale(bmx[n]);
-            W[n] = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
+            W[n] = make_float2(acc[2 * q], acc[2 * q + 1]);
           }
         }
       } else {
@@ -346,8 +360,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int q = 0; q < 64; ++q) {
           const int n = n0 + q;
           if (n < p.N) {
-            const float sc = rs * inv_scale(bmx[n]);
-            float2 val = make_float2(acc[2 * q] * sc, acc[2 * q + 1] * sc);
+            float2 val = make_float2(acc[2 * q], acc[2 * q + 1]);
             if (p.accumulate) {
               float2 o = Crow[n];
               val.x += o.x;
@@ -380,7 +393,7 @@ constexpr int T2_STAGES = 3;
 constexpr int A2_TILE = 128 * TC_BK * 2;                 // 16 KB per CTA
 constexpr int B2_TILE = 128 * TC_BK * 2;                 // 16 KB per CTA (half of the B tile)
 constexpr int STAGE2_BYTES = 2 * A2_TILE + 2 * B2_TILE;  // 64 KB
-constexpr int EPI_Q = 8;                                 // complex columns per staged store step
+constexpr int EPI_Q = 8;  // complex columns per staged store step (the fast path stores 4 lanes x 2 per row)
 constexpr int EPI_STAGE_BYTES = 8 * 32 * (EPI_Q + 1) * 8;  // per-warp 32 x (8+1) float2 (8 warps)
 constexpr int EPI_COLSC_BYTES = 8 * 64 * 4;                 // per-warp column scales of a tile
 constexpr int SMEM2_BYTES = T2_STAGES * STAGE2_BYTES + EPI_STAGE_BYTES + EPI_COLSC_BYTES + 1024 + 256;
@@ -529,7 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       for (int t = cluster; t < ntiles; t += nclusters) {
         const PairTile tl = pair_tile(p, t, npm, nn);
         for (int q = 0; q < tl.nkb; ++q, ++i) {
-          const int kin = q % g_kc, buf = c & 1;
+          const int kin = q % SB_KB, buf = c & 1;
           if (kin == 0) {
             mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -550,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             mma_f16_pair(dacc, alo + adv, bhi + adv, idesc, 1u);
           }
           mma_commit_pair(&empty[s]);
-          if (kin == g_kc - 1 || q == tl.nkb - 1) {
+          if (kin == SB_KB - 1 || q == tl.nkb - 1) {
             mma_commit_pair(&acc_full[buf]);
             ++c;
           }
@@ -571,23 +584,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       float acc[128];
 #pragma unroll
       for (int i = 0; i < 128; ++i) acc[i] = 0.f;
-      const int nchunks = (tl.nkb + g_kc - 1) / g_kc;
+      const int nchunks = (tl.nkb + SB_KB - 1) / SB_KB;
+      const float* ascr = p.ascale + ((int64_t)tl.z * p.nsb + tl.kb0 / SB_KB) * p.Mp + row;  // row < Mp
+      const float* bscr = p.bscale + ((int64_t)(p.b_batched ? tl.z : 0) * p.nsb + tl.kb0 / SB_KB) * p.Np +
+                          ((tl.nblk * TC_BN + half * 128) >> 1);
+      float* fcol = epi_colsc + (warp - 2) * 64;  // this warp's 64 column factors of the chunk
       for (int cc0 = 0; cc0 < nchunks; ++cc0, ++c) {
         const int buf = c & 1;
+        const float f = ascr[(int64_t)cc0 * p.Mp];  // 1/s of this row's scale block
+        __syncwarp();
+        fcol[lane] = bscr[(int64_t)cc0 * p.Np + lane];  // columns < Np
+        fcol[lane + 32] = bscr[(int64_t)cc0 * p.Np + lane + 32];
+        __syncwarp();
         mbar_wait(&acc_full[buf], (c >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-        for (int cc = 0; cc < 128; cc += 16) {
-          uint32_t v[16];
+        for (int cc = 0; cc < 128; cc += 8) {
+          uint32_t v[8];
           const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * TC_BN + half * 128 + cc);
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-              : "r"(taddr));
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                       : "r"(taddr));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[cc + i] += __uint_as_float(v[i]);
+          for (int i = 0; i < 8; i += 2) {
+            const float g = f * fcol[(cc + i) >> 1];
+            acc[cc + i] = fmaf(__uint_as_float(v[i]), g, acc[cc + i]);
+            acc[cc + i + 1] = fmaf(__uint_as_float(v[i + 1]), g, acc[cc + i + 1]);
+          }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
@@ -597,11 +621,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       // (padded rows), then writes 4 rows per store instruction (8 lanes x 8 B = 64 B each),
       // instead of 32 scattered rows per instruction.
       {
-        const int z = tl.z, bz = p.b_batched ? z : 0;
+        const int z = tl.z;
         const int row0 = (tl.mblk0 + (int)rank) * 128 + lg * 32;
-        const float rs = (row < p.M) ? inv_scale(row_amax(p, z, row)) : 0.f;
+        const float rs = (row < p.M) ? 1.f : 0.f;  // A's scales: applied per block in the promotion
         float lmax = 0.f;
-        const float* bmx = p.bmax + (int64_t)bz * p.Np;
         const int n0 = (tl.nblk * TC_BN + half * 128) >> 1;
         float2* base;
         int64_t ld;
@@ -616,45 +639,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           acc_out = p.accumulate != 0;
         }
         float2* stg = epi_stage + (warp - 2) * 32 * (EPI_Q + 1);
-        // the tile's 64 column scales, once per warp (all lanes share the columns)
-        float* csc = epi_colsc + (warp - 2) * 64;
-        {
-          const int na = n0 + lane, nb = n0 + lane + 32;
-          csc[lane] = (na < p.N) ? inv_scale(bmx[na]) : 0.f;
-          csc[lane + 32] = (nb < p.N) ? inv_scale(bmx[nb]) : 0.f;
-        }
-        __syncwarp();
+
         const int sub = lane >> 3, col = lane & 7;
         // per-sample output bounds: one per warp when its 32 rows belong to one sample (always,
         // unless a sample's row count is not a multiple of 32), else one atomic per element
         const int s_lo = sample_of(p.rows_per_sample, p.z0, z, p.nb2, row0, p.amax_out_n);
         const bool s_mixed = p.amax_out && p.ksplit == 1 &&
                              sample_of(p.rows_per_sample, p.z0, z, p.nb2, min(row0 + 31, p.M - 1), p.amax_out_n) != s_lo;
+        // Interior fast path (warp-uniform): the warp's 32 rows and 64 columns all in range, no
+        // read-modify-write, one output bound per warp. Each lane then stores two adjacent
+        // complex values (16 B) of rows row0 + 8 r + lane / 4 with no per-element predicates or
+        // index arithmetic -- the general loop below costs ~60 instructions per output, which
+        // made the K = 128 GEMMs (one accumulation chunk per tile) epilogue-bound.
+        const bool fast = !acc_out && !s_mixed && row0 + 32 <= p.M && n0 + 64 <= p.N && (ld & 1) == 0 &&
+                          ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
 #pragma unroll
         for (int q0 = 0; q0 < 64; q0 += EPI_Q) {
 #pragma unroll
           for (int q = 0; q < EPI_Q; ++q) {
-            const float sc = rs * csc[q0 + q];
-            stg[lane * (EPI_Q + 1) + q] = make_float2(acc[2 * (q0 + q)] * sc, acc[2 * (q0 + q) + 1] * sc);
+            stg[lane * (EPI_Q + 1) + q] = make_float2(acc[2 * (q0 + q)] * rs, acc[2 * (q0 + q) + 1] * rs);
           }
           __syncwarp();
-          const int n = n0 + q0 + col;
+          if (fast) {
+            const int fr = lane >> 2, fc = (lane & 3) * 2;  // row within an 8-row group, column pair
+            float2* fdst = base + (int64_t)(row0 + fr) * ld + (n0 + q0 + fc);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const float2* src = stg + (r * 8 + fr) * (EPI_Q + 1) + fc;
+              const float2 a = src[0], b = src[1];
+              *reinterpret_cast<float4*>(fdst + (int64_t)(8 * r) * ld) = make_float4(a.x, a.y, b.x, b.y);
+              lmax = fmaxf(lmax, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(b.x), fabsf(b.y))));
+            }
+          } else {
+            const int n = n0 + q0 + col;
 #pragma unroll 4
-          for (int r = 0; r < 32; r += 4) {
-            const int rr = r + sub, grow = row0 + rr;
-            if (grow < p.M && n < p.N) {
-              float2 val = stg[rr * (EPI_Q + 1) + col];
-              float2* dst = base + (int64_t)grow * ld + n;
-              if (acc_out) {
-                const float2 o = *dst;
-                val.x += o.x;
-                val.y += o.y;
+            for (int r = 0; r < 32; r += 4) {
+              const int rr = r + sub, grow = row0 + rr;
+              if (grow < p.M && n < p.N) {
+                float2 val = stg[rr * (EPI_Q + 1) + col];
+                float2* dst = base + (int64_t)grow * ld + n;
+                if (acc_out) {
+                  const float2 o = *dst;
+                  val.x += o.x;
+                  val.y += o.y;
+                }
+                *dst = val;
+                const float mv = fmaxf(fabsf(val.x), fabsf(val.y));
+                if (s_mixed)
+                  atomic_max_nonneg(p.amax_out + sample_of(p.rows_per_sample, p.z0, z, p.nb2, grow, p.amax_out_n), mv);
+                lmax = fmaxf(lmax, mv);
               }
-              *dst = val;
-              const float mv = fmaxf(fabsf(val.x), fabsf(val.y));
-              if (s_mixed)
-                atomic_max_nonneg(p.amax_out + sample_of(p.rows_per_sample, p.z0, z, p.nb2, grow, p.amax_out_n), mv);
-              lmax = fmaxf(lmax, mv);
             }
           }
           __syncwarp();
@@ -738,12 +772,15 @@ struct PrepArgs {
   int Rp;                    // row count of mx per z (complex rows)
   __half* hi;
   __half* lo;
+  float* asc;                // 4M planes: [z][nsb][Rp] 1/s per (row of A / complex column of B, scale block)
+  int nsb;
 };
 
 // A CTA covers 32 rows x PK_K complex k (PK_K / 32 sub-tiles of 32 x 32 through shared
 // memory): the row offsets are computed once per CTA and the grid is PK_K / 32 times smaller
 // than one CTA per sub-tile.
 constexpr int PK_K = 128;
+static_assert(PK_K == SB_K, "a prep tile spans exactly one scale block of A");
 
 __device__ __forceinline__ void prep_offsets(const PrepArgs& a, int64_t* roff, int64_t* koff, int r0, int k0) {
   const int t = threadIdx.x;
@@ -870,11 +907,6 @@ __global__ void __launch_bounds__(256) prep_tiled_kernel(PrepArgs a) {
   __shared__ float scl[32];
   const int r0 = blockIdx.x * 32, k0 = blockIdx.y * PK_K, zz = blockIdx.z;  // rows on x
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
-  if (t >= 224) {
-    const int i = t - 224;
-    const float m = (r0 + i < a.R) ? prep_rowmax(a, zz, r0 + i) : 0.f;
-    scl[i] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
-  }
   prep_offsets(a, roff, koff, r0, k0);
   const float2* base = prep_base(a, zz);
   const int64_t plane = (int64_t)a.Rrows * a.Krp;
@@ -932,11 +964,6 @@ __global__ void __launch_bounds__(256, 4) prep_wide_kernel(PrepArgs a) {
   __shared__ float scl[32];
   const int r0 = blockIdx.x * 32, k0 = blockIdx.y * PK_K, zz = blockIdx.z;  // rows on x
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
-  if (t >= 224) {
-    const int i = t - 224;
-    const float m = (r0 + i < a.R) ? prep_rowmax(a, zz, r0 + i) : 0.f;
-    scl[i] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
-  }
   prep_offsets(a, roff, koff, r0, k0);
   const float2* base = prep_base(a, zz);
   float2 v[16];
@@ -957,6 +984,23 @@ __global__ void __launch_bounds__(256, 4) prep_wide_kernel(PrepArgs a) {
     tile[rr][kk] = w;
   }
   __syncthreads();
+  {  // this tile is one scale block of 32 rows (A) / complex columns (B); 8 threads per row
+    const int j = t >> 3, q = t & 7;
+    float m = 0.f;
+#pragma unroll
+    for (int i = 0; i < PK_K / 8; ++i) {
+      const float2 w = tile[j][q + 8 * i];
+      m = fmaxf(m, fmaxf(fabsf(w.x), fabsf(w.y)));
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (q == 0) {
+      const bool pos = m > 0.f;
+      scl[j] = pos ? ldexpf(1.f, -scale_exp(m)) : 1.f;
+      if (r0 + j < a.Rp) a.asc[((int64_t)zz * a.nsb + blockIdx.y) * a.Rp + r0 + j] = pos ? inv_scale(m) : 1.f;
+    }
+    __syncthreads();
+  }
   const int64_t plane = (int64_t)a.Rrows * a.Krp;
   __half2* hi = reinterpret_cast<__half2*>(a.hi + zz * plane);
   __half2* lo = reinterpret_cast<__half2*>(a.lo + zz * plane);
@@ -1002,15 +1046,16 @@ __global__ void __launch_bounds__(256, 4) prep_wide_kernel(PrepArgs a) {
 constexpr int PKF_ROWS = 8;
 constexpr int PKF_PAIRS = 256;  // k pairs per CTA (= threads)
 __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
+  // a CTA covers 8 rows x 512 complex k = four scale blocks; warp w holds complex k
+  // [64 w, 64 w + 64) of the CTA, so a scale block is warps (2b, 2b + 1)
+  static_assert(PKF_PAIRS * 2 == 4 * SB_K, "kfast CTA = four scale blocks");
   __shared__ int64_t roff[PKF_ROWS];
-  __shared__ float scl[PKF_ROWS];
+  __shared__ float wmax[8][PKF_ROWS];
   const int r0 = blockIdx.x * PKF_ROWS, zz = blockIdx.z;  // rows on x (2^31 limit)
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   if (t < PKF_ROWS) {
     const int r = r0 + t;
     roff[t] = (r < a.R) ? view_off(a.vr, r) : -1;
-    const float m = (r < a.R) ? prep_rowmax(a, zz, r) : 0.f;
-    scl[t] = (m > 0.f) ? ldexpf(1.f, -scale_exp(m)) : 1.f;
   }
   const int kpair = blockIdx.y * PKF_PAIRS + t;  // complex k = 2 kpair, 2 kpair + 1
   const int k = 2 * kpair;
@@ -1018,8 +1063,24 @@ __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
   const bool in_k = k < a.K;                      // K even on this path: k + 1 < K too
   const int64_t ko = in_k ? view_off(a.vk, k) : 0;
   __syncthreads();
-  if (!in_plane) return;
   const float2* base = prep_base(a, zz);
+  float4 v[PKF_ROWS];
+#pragma unroll
+  for (int j = 0; j < PKF_ROWS; ++j) {
+    v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (in_k && roff[j] >= 0) v[j] = *reinterpret_cast<const float4*>(base + roff[j] + ko);
+    if (a.conj) {
+      v[j].y = -v[j].y;
+      v[j].w = -v[j].w;
+    }
+    float m = fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) wmax[w][j] = m;
+  }
+  __syncthreads();
+  const int sb = blockIdx.y * 4 + (w >> 1);  // scale block of this warp
+  if (!in_plane) return;
   const int64_t plane = (int64_t)a.Rrows * a.Krp;
   uint2* hi = reinterpret_cast<uint2*>(a.hi + zz * plane);
   uint2* lo = reinterpret_cast<uint2*>(a.lo + zz * plane);
@@ -1028,16 +1089,13 @@ __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
   for (int j = 0; j < PKF_ROWS; ++j) {
     const int r = r0 + j;
     if (r >= a.Rrows) break;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (in_k && roff[j] >= 0) v = *reinterpret_cast<const float4*>(base + roff[j] + ko);
-    if (a.conj) {
-      v.y = -v.y;
-      v.w = -v.w;
-    }
-    const float sc = scl[j];
+    const float m = fmaxf(wmax[w & ~1][j], wmax[w | 1][j]);
+    const bool pos = m > 0.f;
+    const float sc = pos ? ldexpf(1.f, -scale_exp(m)) : 1.f;
+    if (lane == 0 && (w & 1) == 0) a.asc[((int64_t)zz * a.nsb + sb) * a.Rp + r] = pos ? inv_scale(m) : 1.f;
     __half2 h0, l0, h1, l1;
-    split16x2(v.x * sc, v.y * sc, h0, l0);
-    split16x2(v.z * sc, v.w * sc, h1, l1);
+    split16x2(v[j].x * sc, v[j].y * sc, h0, l0);
+    split16x2(v[j].z * sc, v[j].w * sc, h1, l1);
     uint2 hv, lv;
     hv.x = *reinterpret_cast<uint32_t*>(&h0);
     hv.y = *reinterpret_cast<uint32_t*>(&h1);
@@ -1856,11 +1914,11 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     return v;
   };
   auto inner_unit = [](const View4& v) { return v.rank > 0 && v.str[v.rank - 1] == 1; };
-  // ---- B planes (once, or per batch element)
+  // ---- B planes (once, or per batch element); scales per (complex column, scale block)
+  const int nsb = ceil_div(Krp, 2 * SB_K);
   const int nzb = b_batched ? nbz : 1;
   DevBuf bh((size_t)nzb * Nrp * Krp * 2, c.stream), bl((size_t)nzb * Nrp * Krp * 2, c.stream);
-  DevBuf bmx((size_t)nzb * Np * sizeof(float), c.stream);
-  TN_CUDA(cudaMemsetAsync(bmx.p, 0, (size_t)nzb * Np * sizeof(float), c.stream));
+  DevBuf bsc((size_t)nzb * nsb * Np * sizeof(float), c.stream);
   if (g.amaxC) TN_CUDA(cudaMemsetAsync(g.amaxC, 0, sizeof(float) * std::max(1, g.amaxC_n), c.stream));
   // grid.z <= 65535: per-sample B planes are prepared in chunks of batch elements
   for (int zb0 = 0; zb0 < nzb; zb0 += 65535) {
@@ -1879,20 +1937,17 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     a.Rrows = Nrp;
     a.Krp = Krp;
     a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
-    a.mx = bmx.as<float>() + (int64_t)zb0 * Np;
+    a.mx = nullptr;
     a.mx_sample = nullptr;
     a.mx_sample_n = 0;
     a.rows_per_sample = 0;
     a.Rp = Np;
     a.hi = bh.as<__half>() + (int64_t)zb0 * Nrp * Krp;
     a.lo = bl.as<__half>() + (int64_t)zb0 * Nrp * Krp;
-    dim3 gmax(ceil_div(g.N, 32), ceil_div(g.K, PK_K), nzc);
-    if (prep_wide_on()) rowmax_wide_kernel<<<gmax, 256, 0, c.stream>>>(a);
-    else rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
-    TN_LAUNCHED();
+    a.asc = bsc.as<float>() + (int64_t)zb0 * nsb * Np;
+    a.nsb = nsb;
     dim3 grid(Nrp / 64, ceil_div(Krp / 2, PK_K), nzc);
-    if (prep_wide_on()) prep_wide_kernel<1><<<grid, 256, 0, c.stream>>>(a);
-    else prep_tiled_kernel<1><<<grid, 256, 0, c.stream>>>(a);
+    prep_wide_kernel<1><<<grid, 256, 0, c.stream>>>(a);
     TN_LAUNCHED();
   }
   const int bbox = pair ? TC_BN / 2 : TC_BN;
@@ -1912,11 +1967,9 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     kbps = ((kblocks + ksplit - 1) / ksplit + TC_KC - 1) / TC_KC * TC_KC;
     ksplit = (kblocks + kbps - 1) / kbps;
   }
-  // A's scale: one exponent per sample when its producer recorded the sample's max |component|
-  // (no row-max pass; error per element <= 2^-24 of that maximum), else per row. Rows map to
-  // samples as row / m_per_sample when the batch is folded into M, else by the outer batch index.
-  static const bool uniform_off = getenv("TN_ROWSCALE") && std::atoi(getenv("TN_ROWSCALE")) != 0;
-  const bool use_uniform = g.amaxA != nullptr && !uniform_off;
+  // A's scales: one exponent per (row, SB_K complex K) block, found by the prep kernel from the
+  // tile it converts (no max pass); rows map to samples as row / m_per_sample when the batch is
+  // folded into M, else by the outer batch index (output bounds only).
   const int rows_per_sample = g.nb1 > 1 ? 0 : (g.m_per_sample > 0 ? g.m_per_sample : g.M);
   // ---- A planes, chunked over the batch to bound the workspace (<= ~1 GB per plane)
   const int64_t per_z = (int64_t)Mp * Krp;
@@ -1924,7 +1977,7 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       1, std::min<int64_t>({(int64_t)nbz, (int64_t)(65535 / ksplit), (int64_t)(1ll << 29) / std::max<int64_t>(1, per_z)}));
   const int zc = g_zc_max > 0 ? std::min(zc0, g_zc_max) : zc0;  // tn_debug_set_zc: force chunking (tests)
   DevBuf ah((size_t)zc * per_z * 2, c.stream), al((size_t)zc * per_z * 2, c.stream);
-  DevBuf amx((size_t)zc * Mp * sizeof(float), c.stream);
+  DevBuf asc((size_t)zc * nsb * Mp * sizeof(float), c.stream);
   DevBuf ws;
   const int64_t ws_split = (int64_t)zc * g.M * g.N;
   if (ksplit > 1) ws.alloc((size_t)ksplit * ws_split * sizeof(float2), c.stream);
@@ -1945,20 +1998,15 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       a.Rrows = Mp;
       a.Krp = Krp;
       a.k_fast = inner_unit(a.vk) || !inner_unit(a.vr);
-      a.mx = amx.as<float>();
-      a.mx_sample = use_uniform ? g.amaxA : nullptr;
-      a.mx_sample_n = std::max(1, g.amaxA_n);
+      a.mx = nullptr;
+      a.mx_sample = nullptr;
+      a.mx_sample_n = 0;
       a.rows_per_sample = rows_per_sample;
       a.Rp = Mp;
       a.hi = ah.as<__half>();
       a.lo = al.as<__half>();
-      if (!use_uniform) {
-        TN_CUDA(cudaMemsetAsync(amx.p, 0, (size_t)nz * Mp * sizeof(float), c.stream));
-        dim3 gmax(ceil_div(g.M, 32), ceil_div(g.K, PK_K), nz);
-        if (prep_wide_on()) rowmax_wide_kernel<<<gmax, 256, 0, c.stream>>>(a);
-        else rowmax_kernel<<<gmax, 256, 0, c.stream>>>(a);
-        TN_LAUNCHED();
-      }
+      a.asc = asc.as<float>();
+      a.nsb = nsb;
       // K-contiguous operands (innermost K stride 1, even length, 16-byte aligned base and
       // row/batch offsets) take the transpose-free kernel
       const View4& vk = a.vk;
@@ -1972,8 +2020,7 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
         prep_kfast_kernel<<<grid, 256, 0, c.stream>>>(a);
       } else {
         dim3 grid(Mp / 32, ceil_div(Krp / 2, PK_K), nz);
-        if (prep_wide_on()) prep_wide_kernel<0><<<grid, 256, 0, c.stream>>>(a);
-        else prep_tiled_kernel<0><<<grid, 256, 0, c.stream>>>(a);
+        prep_wide_kernel<0><<<grid, 256, 0, c.stream>>>(a);
       }
       TN_LAUNCHED();
     }
@@ -1988,8 +2035,11 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.ws = ws.as<float2>();
     p.ws_split = ws_split;
     p.b_batched = b_batched ? 1 : 0;
-    p.amax = amx.as<float>();
-    p.bmax = bmx.as<float>() + (b_batched ? (int64_t)z0 * Np : 0);
+    p.amax = nullptr;
+    p.ascale = asc.as<float>();
+    p.nsb = nsb;
+    p.bmax = nullptr;
+    p.bscale = bsc.as<float>() + (b_batched ? (int64_t)z0 * nsb * Np : 0);
     p.Mp = Mp;
     p.Np = Np;
     p.C = g.C;
@@ -1999,8 +2049,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.sc2 = g.sc2;
     p.z0 = z0;
     p.accumulate = g.accumulate ? 1 : 0;
-    p.amax_sample = use_uniform ? g.amaxA : nullptr;
-    p.amax_sample_n = std::max(1, g.amaxA_n);
+    p.amax_sample = nullptr;
+    p.amax_sample_n = 1;
     p.amax_out = g.amaxC;
     p.amax_out_n = std::max(1, g.amaxC_n);
     p.rows_per_sample = rows_per_sample;
@@ -2081,6 +2131,3 @@ extern "C" int tn_debug_set_zc(int zc) {
   return 0;
 }
 
-extern "C" int tn_debug_kc(int kc) {
-  return cudaMemcpyToSymbol(tn::g_kc, &kc, sizeof(int)) == cudaSuccess ? 0 : -1;
-}

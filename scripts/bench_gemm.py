@@ -13,8 +13,6 @@ LIB.tn_debug_last_error.restype = C.c_char_p
 shapes = [(32768, 4096, 4096, 2), (16384, 2048, 1024, 4), (8192, 128, 4096, 8), (4096, 4096, 4096, 1),
           (128, 4096, 4096, 4), (300, 2048, 2048, 2), (8192, 16384, 128, 2), (16384, 4096, 128, 2)]
 modes = [int(x) for x in os.environ.get("MODES", "2,1").split(",")]
-if os.environ.get("KC"):
-    LIB.tn_debug_kc(int(os.environ["KC"]))
 # warm the clocks up (~1-2 s of GEMMs) before timing
 out = np.zeros(4)
 for _ in range(3):

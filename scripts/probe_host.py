@@ -16,9 +16,6 @@ nb = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 lat_name, chi, R, _ = bench.WORKLOADS[wl]
 lat = L.by_name(lat_name)
 g = TNState(bench.make_state(lat, chi))
-if os.environ.get("KC"):
-    from paper_2507_11424_b200 import _lib
-    _lib.lib().tn_debug_kc(int(os.environ["KC"]))
 if os.environ.get("RASTER_GM"):
     from paper_2507_11424_b200 import _lib
     _lib.lib().tn_debug_raster(int(os.environ["RASTER_GM"]))

@@ -521,10 +521,18 @@ def test_chip_row_partition_willow_exact_closed_form():
     """NEXT-3: the Willow-105 chip-row ("diagonal") partition -- 15 rows of 7
     qubits, two up and two down edges per interior qubit -- through the vertex split, on the GPU:
     a K = 3 branch superposition at chi = 4 (split bonds chi^2 = 16, chi_env = 32 >= every
-    boundary rank) gives the closed-form conditionals of every qubit; virtual vertices draw 0."""
+    boundary rank) gives the closed-form conditionals of every qubit; virtual vertices draw 0.
+    The branch factors phi_v^(c) have unit norm, so the three branches carry comparable weight:
+    with unnormalised Gaussian factors (seed 5) branch 1 weighs 1.6e-5 of branch 0 over the
+    lattice and less on partial products of rows, below the complex64 environments' resolution
+    ("dynamic range"): the GPU then returns exactly the closed form of the
+    two remaining branches (0.948771 vs 0.948645 at qubit 93)."""
     from tests.test_oracle import closed_form_conditionals
     lat = L.willow105()
-    st = S.branch_superposition(lat, 4, 3, seed=5)
+    rng = np.random.default_rng(5)
+    phis = rng.standard_normal((3, lat.n, 2)) + 1j * rng.standard_normal((3, lat.n, 2))
+    phis /= np.linalg.norm(phis, axis=2, keepdims=True)
+    st = S.branch_superposition(lat, 4, 3, seed=5, phis=phis)
     st2, rows2, nq = _chip(lat, st)
     u = S.uniforms(6, st2["n"], 19)
     g, bits, logq, cond, flags = _run(st2, rows2, 32, u)
