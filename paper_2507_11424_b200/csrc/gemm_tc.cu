@@ -1065,6 +1065,7 @@ __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
   __syncthreads();
   const float2* base = prep_base(a, zz);
   float4 v[PKF_ROWS];
+  float m8[PKF_ROWS];
 #pragma unroll
   for (int j = 0; j < PKF_ROWS; ++j) {
     v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1073,11 +1074,29 @@ __global__ void __launch_bounds__(256) prep_kfast_kernel(PrepArgs a) {
       v[j].y = -v[j].y;
       v[j].w = -v[j].w;
     }
-    float m = fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w)));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) wmax[w][j] = m;
+    m8[j] = fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w)));
   }
+  // warp max of the 8 rows in 9 shuffles: halve the rows per lane while doubling the lanes
+  // covered (offsets 16, 8, 4), then reduce the remaining row over 4 lanes
+  static_assert(PKF_ROWS == 8, "row-halving reduction assumes 8 rows");
+  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+  float m4[4], m2[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = u16 ? m8[i] : m8[i + 4];
+    const float keep = u16 ? m8[i + 4] : m8[i];
+    m4[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = u8 ? m4[i] : m4[i + 2];
+    const float keep = u8 ? m4[i + 2] : m4[i];
+    m2[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+  }
+  float m1 = fmaxf(u4 ? m2[1] : m2[0], __shfl_xor_sync(0xffffffffu, u4 ? m2[0] : m2[1], 4));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+  if ((lane & 3) == 0) wmax[w][(u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0)] = m1;
   __syncthreads();
   const int sb = blockIdx.y * 4 + (w >> 1);  // scale block of this warp
   if (!in_plane) return;
