@@ -708,37 +708,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 }
 
 // Deterministic split-K reduction: C (+)= sum over splits in a fixed order.
-__global__ void splitk_reduce_kernel(const float2* __restrict__ ws, int ksplit, int64_t ws_split, int nz, int M,
-                                     int N, float2* C, int64_t cm, int nb2, int64_t sc1, int64_t sc2, int z0,
-                                     int accumulate, float* amax_out, int amax_out_n, int rows_per_sample) {
-  const int64_t per = (int64_t)M * N, tot = per * nz;
+// One block per output row (z, row): its N complex values, summed over the splits in order.
+__global__ void __launch_bounds__(128) splitk_reduce_kernel(const float2* __restrict__ ws, int ksplit,
+                                                            int64_t ws_split, int nz, int M, int N, float2* C,
+                                                            int64_t cm, int nb2, int64_t sc1, int64_t sc2, int z0,
+                                                            int accumulate, float* amax_out, int amax_out_n,
+                                                            int rows_per_sample) {
+  const int64_t line = blockIdx.x;  // zz * M + row
+  const int zz = (int)(line / M), row = (int)(line - (int64_t)zz * M);
+  const int z = z0 + zz;
+  const int b1 = z / nb2, b2 = z - b1 * nb2;
+  const float2* w = ws + line * N;
+  float2* cp = C + b1 * sc1 + b2 * sc2 + (int64_t)row * cm;
   float lmax = 0.f;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t zz = e / per, r = e - zz * per;
-    const int row = (int)(r / N), n = (int)(r - (int64_t)row * N);
-    float2 s = ws[e];
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    float2 s = w[n];
     for (int k = 1; k < ksplit; ++k) {
-      const float2 v = ws[k * ws_split + e];
+      const float2 v = w[k * ws_split + n];
       s.x += v.x;
       s.y += v.y;
     }
-    const int z = z0 + (int)zz;
-    const int b1 = z / nb2, b2 = z - b1 * nb2;
-    float2* cp = C + b1 * sc1 + b2 * sc2 + (int64_t)row * cm + n;
     if (accumulate) {
-      const float2 o = *cp;
+      const float2 o = cp[n];
       s.x += o.x;
       s.y += o.y;
     }
-    *cp = s;
-    const float mv = fmaxf(fabsf(s.x), fabsf(s.y));
-    if (amax_out && amax_out_n > 1)
-      atomic_max_nonneg(amax_out + sample_of(rows_per_sample, z0, (int)zz, nb2, row, amax_out_n), mv);
-    lmax = fmaxf(lmax, mv);
+    cp[n] = s;
+    lmax = fmaxf(lmax, fmaxf(fabsf(s.x), fabsf(s.y)));
   }
-  if (amax_out && amax_out_n <= 1) {
+  if (amax_out) {  // output bounds (only the 3M path's consumers use them)
     lmax = warp_max(lmax);
-    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(amax_out, lmax);
+    if ((threadIdx.x & 31) == 0)
+      atomic_max_nonneg(amax_out + sample_of(rows_per_sample, z0, zz, nb2, row, amax_out_n), lmax);
   }
 }
 
@@ -1852,9 +1853,8 @@ void gemm_tc3m(Ctx& c, const GemmDesc& g, int dev, cudaEvent_t ev_kernel) {
       TN_LAUNCHED();
     }
     if (ksplit > 1) {
-      int64_t tot = (int64_t)nz * g.M * g.N;
-      unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16);
-      splitk_reduce_kernel<<<blocks, 256, 0, c.stream>>>(p.ws, ksplit, ws_split, nz, g.M, g.N, g.C, g.cm, g.nb2,
+      const unsigned blocks = (unsigned)((int64_t)nz * g.M);
+      splitk_reduce_kernel<<<blocks, 128, 0, c.stream>>>(p.ws, ksplit, ws_split, nz, g.M, g.N, g.C, g.cm, g.nb2,
                                                          g.sc1, g.sc2, z0, p.accumulate, g.amaxC, p.amax_out_n,
                                                          rows_per_sample);
       TN_LAUNCHED();
@@ -1872,6 +1872,10 @@ int m3_mode() {
   static const int m = getenv("TN_3M") ? std::atoi(getenv("TN_3M")) : 0;
   return m;
 }
+
+// Output bounds (GemmDesc::amaxC) feed only the 3M path's per-sample A scales; the 4M path
+// scales A per (row, block) from the data itself.
+bool tc_bounds_wanted() { return (g_m3_override >= 0 ? g_m3_override : m3_mode()) != 0; }
 
 bool gemm_tc(Ctx& c, const GemmDesc& g) {
   if (!tc_eligible(c, g.M, g.N, g.K, g.work_per_sample)) return false;
@@ -2123,9 +2127,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       TN_LAUNCHED();
     }
     if (ksplit > 1) {
-      int64_t tot = (int64_t)nz * g.M * g.N;
-      unsigned blocks = (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16);
-      splitk_reduce_kernel<<<blocks, 256, 0, c.stream>>>(p.ws, ksplit, ws_split, nz, g.M, g.N, g.C, g.cm, g.nb2,
+      const unsigned blocks = (unsigned)((int64_t)nz * g.M);
+      splitk_reduce_kernel<<<blocks, 128, 0, c.stream>>>(p.ws, ksplit, ws_split, nz, g.M, g.N, g.C, g.cm, g.nb2,
                                                          g.sc1, g.sc2, z0, p.accumulate, g.amaxC, p.amax_out_n,
                                                          rows_per_sample);
       TN_LAUNCHED();

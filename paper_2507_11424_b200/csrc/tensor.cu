@@ -726,7 +726,7 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
     g.amaxA = tensor_amax(X, &g.amaxA_n);
     if (g.amaxA_n < (X.bstride ? c.nb : 1)) g.amaxA = nullptr;  // bounds of another batch
   }
-  if (C.mem && !g.accumulate) {
+  if (C.mem && !g.accumulate && tc_bounds_wanted()) {
     g.amaxC = C.mem->make_amax();
     g.amaxC_n = C.mem->tail_n;
   }

@@ -96,6 +96,8 @@ struct GemmDesc {
 };
 // Returns true when the tensor-core path ran (and filled g.amaxC if set).
 bool gemm(Ctx& c, const GemmDesc& g);
+// Whether the tensor-core path uses producers' output bounds (the 3M path only).
+bool tc_bounds_wanted();
 // Whether gemm() will route a GEMM of this per-sample shape to the tensor cores.
 bool tc_eligible(const Ctx& c, int64_t M, int64_t N, int64_t K, int64_t work_per_sample);
 

@@ -376,6 +376,29 @@ def test_gemm_ladder_shape_elementwise():
     assert np.isfinite(out).all()
 
 
+@pytest.mark.parametrize("shape", [(512, 1024, 256), (300, 700, 130), (100, 600, 70)])
+def test_gemm_block_scaling_cancellation(shape):
+    """Per-(row, 128-complex-K block) scales of A and per-(column, block) scales of B: each row
+    of A is O(1) on the first K block and 1e-9 on the rest; B's first block rows are zero for
+    the even columns. C[:, even] then only sees the small blocks (values ~1e-9 of A's row
+    maximum). One scale per row (or per sample) would leave those entries an absolute error
+    ~2^-24 of the row maximum, i.e. O(1) relative; the block scales keep every element within
+    1e-5 of FP64 relative to sum_k |a_k b_k| (tcgen05 forced; ragged M, N, K)."""
+    M, K, N = shape
+    rng = np.random.default_rng(47)
+    A = _rand32(rng, (M, K))
+    A[:, 128:] *= np.float32(1e-9)
+    B = _rand32(rng, (K, N))
+    B[:128, 0::2] = 0
+    out = _contract_only(A, "mk", B, "kn", "mn", (M, N), 1, False, False, gemm=2)
+    Ad, Bd = A.astype(np.complex128), B.astype(np.complex128)
+    ref = Ad @ Bd
+    bound = np.abs(Ad) @ np.abs(Bd)
+    err = (np.abs(out - ref) / bound).max()
+    print("block-scaling cancellation: max |dC| / sum|a||b|", err)
+    assert err <= 1e-5, err
+
+
 @pytest.mark.parametrize("zc", [0, 2, 1])
 def test_gemm_per_sample_b_chunked(zc):
     """Contraction with per-sample B over a batched label (the N = 128 ladder closure Rs =
