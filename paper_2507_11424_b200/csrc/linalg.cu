@@ -589,7 +589,9 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
   double2* lvb = Y;  // [2][CH_MAXN] column buffers (the per-warp scratch is free here)
   __shared__ int s_brk, s_next;
   auto phase_a = [&](int k, int p, const double2* lprev, double2* lcur) {
-    // warp 0 only: column of pivot p (G_k(:,p) = stored column minus the previous step's term)
+    // warp 0 only: column of pivot p (G_k(:,p) = stored column minus the previous step's term).
+    // Lane l owns rows l, l+32, l+64, l+96: all loads are issued first, then the arithmetic,
+    // then the stores, and the next pivot is picked from the updated diagonal on the way.
     double dp = dg[p];
     bool brk = false;
     if (PIVOT) {
@@ -602,45 +604,61 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
     if (!brk) {
       const double inv = rsqrt(dp);
       const double lkk = dp * inv;
-      double2 lpp = make_double2(0, 0);
-      if (lprev) lpp = lprev[p];
-      for (int i = lane; i < n; i += 32) {
-        if (i == p) {
-          S[pk(p, p)] = make_double2(lkk, 0);
-          lcur[i] = make_double2(0, 0);
-        } else if (alive[i]) {
-          double2 g = i > p ? S[pk(i, p)] : S[pk(p, i)];
-          if (i < p) g.y = -g.y;  // G(i, p) = conj(G(p, i))
-          if (lprev) {            // lookahead: step k-1's rank-1 term on column p
-            const double2 li = lprev[i];
-            g.x -= li.x * lpp.x + li.y * lpp.y;
-            g.y -= li.y * lpp.x - li.x * lpp.y;
+      const double2 lpp = lprev ? lprev[p] : make_double2(0, 0);
+      double bv = -1;
+      int bi = n;
+#pragma unroll
+      for (int q0 = 0; q0 < CH_MAXN / 32; q0 += 2) {  // two rows per lane at a time (64 registers)
+        double2 g[2], li[2];
+        double dgi[2];
+        bool act[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * (q0 + h);
+          act[h] = i < n && i != p && alive[i];
+          g[h] = make_double2(0, 0);
+          li[h] = make_double2(0, 0);
+          dgi[h] = 0;
+          if (act[h]) {
+            g[h] = i > p ? S[pk(i, p)] : S[pk(p, i)];
+            if (lprev) li[h] = lprev[i];
+            dgi[h] = dg[i];
           }
-          const double2 l = make_double2(g.x * inv, g.y * inv);
-          lcur[i] = l;
-          if (i > p) S[pk(i, p)] = l;
-          else S[pk(p, i)] = make_double2(l.x, -l.y);
-          dg[i] -= l.x * l.x + l.y * l.y;
-        } else {
-          lcur[i] = make_double2(0, 0);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * (q0 + h);
+          if (i >= n) break;
+          if (act[h]) {
+            double2 gg = g[h];
+            if (i < p) gg.y = -gg.y;  // G(i, p) = conj(G(p, i))
+            if (lprev) {              // lookahead: step k-1's rank-1 term on column p
+              gg.x -= li[h].x * lpp.x + li[h].y * lpp.y;
+              gg.y -= li[h].y * lpp.x - li[h].x * lpp.y;
+            }
+            const double2 l = make_double2(gg.x * inv, gg.y * inv);
+            lcur[i] = l;
+            if (i > p) S[pk(i, p)] = l;
+            else S[pk(p, i)] = make_double2(l.x, -l.y);
+            const double d = dgi[h] - (l.x * l.x + l.y * l.y);
+            dg[i] = d;
+            if (PIVOT && d > bv) {  // increasing i per lane: the first maximum wins ties
+              bv = d;
+              bi = i;
+            }
+          } else {
+            lcur[i] = make_double2(0, 0);
+            if (i == p) S[pk(p, p)] = make_double2(lkk, 0);
+          }
         }
       }
-      __syncwarp();
       if (lane == 0) {
         alive[p] = 0;
         perm[k] = p;
       }
-      __syncwarp();
       // next pivot from the updated diagonal
       if (k + 1 < n) {
         if (PIVOT) {
-          double bv = -1;
-          int bi = n;
-          for (int i = lane; i < n; i += 32)
-            if (alive[i] && dg[i] > bv) {
-              bv = dg[i];
-              bi = i;
-            }
           for (int o = 16; o > 0; o >>= 1) {
             const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
             const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
@@ -649,12 +667,12 @@ __global__ void __launch_bounds__(CH_THREADS) chol_smem_kernel(const double2* __
               bi = oi;
             }
           }
-          nxt = bi < n ? bi : n;
-          if (bi >= n) nxt = n;  // nothing alive: the rank check of the next step stops
+          nxt = bi < n ? bi : n;  // nothing alive: the rank check of the next step stops
         } else {
           nxt = k + 1;
         }
       }
+      __syncwarp();
     }
     if (lane == 0) {
       s_brk = brk ? 1 : 0;
