@@ -83,13 +83,78 @@ struct TcParams {
   const float* ascale;        // 4M kernels: [z][nsb][Mp] 1/s of A's (row, scale block) exponents
   const float* bscale;        // 4M kernels: [zb][nsb][Np] 1/s of B's (column, scale block)
   int nsb;                    // scale blocks (SB_KB k-blocks = SB_K complex K each) along K
+  // plane output (pair kernel, ksplit 1): C is written as the next GEMM's FP16 A planes with
+  // per-(row, block) scales; a CTA's 128 rows are exactly one scale block of that operand
+  int pout;
+  PView pvm, pvn;
+  __half* pho;
+  __half* plo;
+  float* psc;
 };
+
+__device__ __forceinline__ void pview_off(const PView& v, int64_t idx, int64_t& po, int64_t& so) {
+  po = 0;
+  so = 0;
+#pragma unroll
+  for (int d = 3; d >= 0; --d) {
+    if (d < v.rank) {
+      const int64_t q = idx / v.dims[d];
+      const int64_t r = idx - q * v.dims[d];
+      po += r * v.po[d];
+      so += r * v.so[d];
+      idx = q;
+    }
+  }
+}
+
+// Max of |components| of 32 complex columns (acc[2 c0 .. 2 c0 + 63]) over the warp's 32 rows:
+// five halving exchanges (16 + 8 + 4 + 2 + 1 shuffles); lane l returns column c0 + l.
+__device__ __forceinline__ float warp_colmax32(const float* acc, int c0, int lane) {
+  float r16[16];
+  const bool b16 = lane & 16;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float mj = fmaxf(fabsf(acc[2 * (c0 + j)]), fabsf(acc[2 * (c0 + j) + 1]));
+    const float mk = fmaxf(fabsf(acc[2 * (c0 + j + 16)]), fabsf(acc[2 * (c0 + j + 16) + 1]));
+    r16[j] = fmaxf(b16 ? mk : mj, __shfl_xor_sync(0xffffffffu, b16 ? mj : mk, 16));
+  }
+  float r8[8];
+  const bool b8 = lane & 8;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    r8[j] = fmaxf(b8 ? r16[j + 8] : r16[j], __shfl_xor_sync(0xffffffffu, b8 ? r16[j] : r16[j + 8], 8));
+  float r4[4];
+  const bool b4 = lane & 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    r4[j] = fmaxf(b4 ? r8[j + 4] : r8[j], __shfl_xor_sync(0xffffffffu, b4 ? r8[j] : r8[j + 4], 4));
+  float r2[2];
+  const bool b2 = lane & 2;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    r2[j] = fmaxf(b2 ? r4[j + 2] : r4[j], __shfl_xor_sync(0xffffffffu, b2 ? r4[j] : r4[j + 2], 2));
+  const bool b1 = lane & 1;
+  return fmaxf(b1 ? r2[1] : r2[0], __shfl_xor_sync(0xffffffffu, b1 ? r2[0] : r2[1], 1));
+}
 
 // Sample of an M-side row (A's rows and C's rows share the mapping), for bounds of count n.
 __device__ __forceinline__ int sample_of(int rows_per_sample, int z0, int z, int nb2, int row, int n) {
   if (n <= 1) return 0;
   const int s = rows_per_sample > 0 ? row / rows_per_sample : (z0 + z) / nb2;
   return min(s, n - 1);
+}
+
+__device__ __forceinline__ void split16(float x, __half& h, __half& l) {
+  h = __float2half_rn(x);
+  l = __float2half_rn(x - __half2float(h));
+}
+
+__device__ __forceinline__ void split16x2(float x, float y, __half2& h, __half2& l) {
+  __half hx, lx, hy, ly;
+  split16(x, hx, lx);
+  split16(y, hy, ly);
+  h = __halves2half2(hx, hy);
+  l = __halves2half2(lx, ly);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -469,6 +534,7 @@ __device__ __forceinline__ PairTile pair_tile(const TcParams& p, int t, int npm,
   return r;
 }
 
+template <bool POUT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                     const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo, TcParams p,
@@ -616,6 +682,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(acc_empty0 + (uint32_t)(buf * sizeof(uint64_t)));
+      }
+      if (POUT) {
+        // Plane output: the CTA's 128 rows x this half's 64 complex columns; column q of the
+        // tile is one scale block (row of the consumer's A, block of 128 consumer K). Block
+        // maxima: warp column maxima, then the four warps of this half combine them in shared
+        // memory (named barrier 1 + half, 128 threads).
+        const int n0 = (tl.nblk * TC_BN + half * 128) >> 1;
+        const int64_t mrow = (int64_t)(tl.mblk0 + (int)rank) * 128 + lg * 32 + lane;
+        float* slot = epi_colsc + (warp - 2) * 64;
+        const float cA = warp_colmax32(acc, 0, lane), cB = warp_colmax32(acc, 32, lane);
+        __syncwarp();
+        slot[lane] = cA;
+        slot[lane + 32] = cB;
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
+        float mA = 0.f, mB = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const float* o = epi_colsc + (half * 4 + w) * 64;
+          mA = fmaxf(mA, o[lane]);
+          mB = fmaxf(mB, o[lane + 32]);
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
+        const float sA = mA > 0.f ? ldexpf(1.f, -scale_exp(mA)) : 1.f;
+        const float sB = mB > 0.f ? ldexpf(1.f, -scale_exp(mB)) : 1.f;
+        int64_t pm, sm, pnA, snA, pnB, snB;
+        pview_off(p.pvm, mrow, pm, sm);
+        pview_off(p.pvn, n0 + lane, pnA, snA);
+        pview_off(p.pvn, n0 + lane + 32, pnB, snB);
+        if (lg == 0) {  // one writer per block: sm is the same for the CTA's 128 rows
+          p.psc[sm + snA] = mA > 0.f ? inv_scale(mA) : 1.f;
+          p.psc[sm + snB] = mB > 0.f ? inv_scale(mB) : 1.f;
+        }
+        __half2* hi = reinterpret_cast<__half2*>(p.pho);
+        __half2* lo = reinterpret_cast<__half2*>(p.plo);
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          const float sc = __shfl_sync(0xffffffffu, q < 32 ? sA : sB, q & 31);
+          const int64_t pn = __shfl_sync(0xffffffffu, q < 32 ? pnA : pnB, q & 31);
+          __half2 h, l;
+          split16x2(acc[2 * q] * sc, acc[2 * q + 1] * sc, h, l);
+          const int64_t off = (pm + pn) >> 1;  // half2 index (complex element)
+          hi[off] = h;
+          lo[off] = l;
+        }
+        continue;
       }
       // Coalesced output: each warp stages 32 rows x 8 complex columns in shared memory
       // (padded rows), then writes 4 rows per store instruction (8 lanes x 8 B = 64 B each),
@@ -885,18 +996,6 @@ __global__ void __launch_bounds__(256, 4) rowmax_wide_kernel(PrepArgs a) {
   }
 }
 
-__device__ __forceinline__ void split16(float x, __half& h, __half& l) {
-  h = __float2half_rn(x);
-  l = __float2half_rn(x - __half2float(h));
-}
-
-__device__ __forceinline__ void split16x2(float x, float y, __half2& h, __half2& l) {
-  __half hx, lx, hy, ly;
-  split16(x, hx, lx);
-  split16(y, hy, ly);
-  h = __halves2half2(hx, hy);
-  l = __halves2half2(lx, ly);
-}
 
 // Pass 2: scaled FP16 hi/lo planes. KIND 0: A planes [z][Rrows][Krp], element (r, 2k+c) =
 // (Re, Im)[c]. KIND 1: B_r^T planes [z][Rrows][Krp], rows 2r = (Re b, -Im b), 2r+1 = (Im b, Re b).
@@ -1842,6 +1941,7 @@ void gemm_tc3m(Ctx& c, const GemmDesc& g, int dev, cudaEvent_t ev_kernel) {
     p.amax_out = g.amaxC;
     p.amax_out_n = std::max(1, g.amaxC_n);
     p.rows_per_sample = rows_per_sample;
+    p.pout = 0;
     if (ev_kernel && z0 == 0) cudaEventRecord(ev_kernel, c.stream);
     {
       ProfScope ps(P_TC_KERNEL, c.stream);
@@ -1912,13 +2012,16 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
   const uint64_t dbit = 1ull << (dev & 63);
   if (!(attr_done.load() & dbit)) {
     TN_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    TN_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+    TN_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+    TN_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
     attr_done.fetch_or(dbit);
   }
   // CTA pairs (M = 256 per cluster) whenever one batch element has more than 128 rows
   static const bool pair_off = getenv("TN_TC2") && std::atoi(getenv("TN_TC2")) == 0;
   const bool pair = !pair_off && g.M > TC_BM;
   const int mm = g_m3_override >= 0 ? g_m3_override : m3_mode();
+  if ((g.po || g.pa) && (!pair || mm != 0))
+    throw Error(-1, "gemm: plane operands need the 4M CTA-pair path");
   if (pair && mm != 0 && (g.K >= 512 || mm == 2)) {
     gemm_tc3m(c, g, dev, slog ? srec.b : nullptr);
     return true;
@@ -1998,15 +2101,25 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
   const int64_t per_z = (int64_t)Mp * Krp;
   const int zc0 = (int)std::max<int64_t>(
       1, std::min<int64_t>({(int64_t)nbz, (int64_t)(65535 / ksplit), (int64_t)(1ll << 29) / std::max<int64_t>(1, per_z)}));
-  const int zc = g_zc_max > 0 ? std::min(zc0, g_zc_max) : zc0;  // tn_debug_set_zc: force chunking (tests)
-  DevBuf ah((size_t)zc * per_z * 2, c.stream), al((size_t)zc * per_z * 2, c.stream);
-  DevBuf asc((size_t)zc * nsb * Mp * sizeof(float), c.stream);
+  int zc = g_zc_max > 0 ? std::min(zc0, g_zc_max) : zc0;  // tn_debug_set_zc: force chunking (tests)
+  if (g.pa) {  // A planes written by the producing GEMM (contract_planes)
+    if (g.pa->Mp != Mp || g.pa->Krp != Krp || g.pa->nsb != nsb || g.pa->nz != nbz)
+      throw Error(-1, "gemm: A planes do not match the GEMM");
+    zc = nbz;
+  }
+  if (g.po && (ksplit != 1 || g.M % (2 * TC_BM) != 0 || g.N % 128 != 0 || nbz != 1))
+    throw Error(-1, "gemm: plane output needs whole tiles and no split-K");
+  DevBuf ah(g.pa ? 0 : (size_t)zc * per_z * 2, c.stream), al(g.pa ? 0 : (size_t)zc * per_z * 2, c.stream);
+  DevBuf asc(g.pa ? 0 : (size_t)zc * nsb * Mp * sizeof(float), c.stream);
   DevBuf ws;
   const int64_t ws_split = (int64_t)zc * g.M * g.N;
   if (ksplit > 1) ws.alloc((size_t)ksplit * ws_split * sizeof(float2), c.stream);
   for (int z0 = 0; z0 < nbz; z0 += zc) {
     const int nz = std::min(zc, nbz - z0);
-    {
+    __half* pah = g.pa ? g.pa->hi->as<__half>() : ah.as<__half>();
+    __half* pal = g.pa ? g.pa->lo->as<__half>() : al.as<__half>();
+    const float* pasc = g.pa ? g.pa->asc->as<float>() : asc.as<float>();
+    if (!g.pa) {
       PrepArgs a;
       a.X = g.A;
       a.vr = g.vam.rank ? g.vam : simple(g.M, g.am);
@@ -2047,8 +2160,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       }
       TN_LAUNCHED();
     }
-    CUtensorMap mah = make_map(ah.as<__half>(), Krp, Mp, nz, TC_BM);
-    CUtensorMap mal = make_map(al.as<__half>(), Krp, Mp, nz, TC_BM);
+    CUtensorMap mah = make_map(pah, Krp, Mp, nz, TC_BM);
+    CUtensorMap mal = make_map(pal, Krp, Mp, nz, TC_BM);
     TcParams p;
     p.M = g.M;
     p.N = g.N;
@@ -2059,8 +2172,17 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.ws_split = ws_split;
     p.b_batched = b_batched ? 1 : 0;
     p.amax = nullptr;
-    p.ascale = asc.as<float>();
+    p.ascale = pasc;
     p.nsb = nsb;
+    p.pout = 0;
+    if (g.po) {
+      p.pout = 1;
+      p.pvm = g.po->vm;
+      p.pvn = g.po->vn;
+      p.pho = g.po->hi;
+      p.plo = g.po->lo;
+      p.psc = g.po->asc;
+    }
     p.bmax = nullptr;
     p.bscale = bsc.as<float>() + (b_batched ? (int64_t)z0 * nsb * Np : 0);
     p.Mp = Mp;
@@ -2108,7 +2230,7 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
           cfg.attrs = &at;
           cfg.numAttrs = 1;
           int n = 0;
-          if (cudaOccupancyMaxActiveClusters(&n, (void*)tc_gemm2_kernel, &cfg) != cudaSuccess || n < 1) {
+          if (cudaOccupancyMaxActiveClusters(&n, (void*)tc_gemm2_kernel<false>, &cfg) != cudaSuccess || n < 1) {
             cudaGetLastError();
             n = 64;
           }
@@ -2118,8 +2240,12 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
         }
         static const bool persist = !(getenv("TN_PERSIST") && std::atoi(getenv("TN_PERSIST")) == 0);
         const int nclusters = persist ? std::min(ntiles, max_clusters) : ntiles;
-        tc_gemm2_kernel<<<2 * nclusters, TC_THREADS, SMEM2_BYTES, c.stream>>>(mah, mal, mb_hi, mb_lo, p, npm, nn,
-                                                                              ntiles);
+        if (p.pout)
+          tc_gemm2_kernel<true><<<2 * nclusters, TC_THREADS, SMEM2_BYTES, c.stream>>>(mah, mal, mb_hi, mb_lo, p, npm,
+                                                                                    nn, ntiles);
+        else
+          tc_gemm2_kernel<false><<<2 * nclusters, TC_THREADS, SMEM2_BYTES, c.stream>>>(mah, mal, mb_hi, mb_lo, p, npm,
+                                                                                     nn, ntiles);
       } else {
         dim3 grid(Nrp / TC_BN, Mp / TC_BM, nz * ksplit);
         tc_gemm_kernel<<<grid, TC_THREADS, SMEM_BYTES, c.stream>>>(mah, mal, mb_hi, mb_lo, p);

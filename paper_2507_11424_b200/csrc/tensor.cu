@@ -513,8 +513,13 @@ std::string order_in(const std::string& lab, const std::string& set) {
 }
 }  // namespace
 
-Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Tensor& B0,
-                const char* lb0, bool conjB0, const char* lout) {
+// Plane-output request of contract_planes: the consumer's batch / row / K labels.
+struct PlaneReq {
+  std::string zl, rl, kl;
+};
+
+static Tensor contract_impl(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Tensor& B0,
+                            const char* lb0, bool conjB0, const char* lout, const PlaneReq* req) {
   // dims of every label
   std::map<char, int> dim;
   auto reg = [&](const Tensor& t, const char* l) {
@@ -572,6 +577,79 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
   for (char ch : Ns) Nsz *= dim[ch];
   for (char ch : Ks) Ksz *= dim[ch];
   bool per_out = X.bstride || Y.bstride;
+  if (Y.planes) throw Error(-1, "contract: a planes operand must be the per-sample left operand");
+  if (X.planes) {
+    // A from the planes its producer wrote: the planes fix the batch, row and K orders
+    const Planes& P = *X.planes;
+    const std::string Kx = order_in(ox.lab, Ks);
+    if (cx || P.lab != std::string(lx) || P.lab != Ls + Ms + Kx || !per_out)
+      throw Error(-1, std::string("contract: planes ") + P.lab + " do not fit " + lx);
+    GemmDesc g;
+    g.M = (int)Msz;
+    g.N = (int)Nsz;
+    g.K = (int)Ksz;
+    g.pa = &P;
+    auto mk = [](const Op& o, const std::string& grp, View4& v) {
+      std::vector<int64_t> d, st;
+      for (char ch : grp) {
+        size_t q = o.lab.find(ch);
+        int64_t dd = o.dims[q], ss = o.str[q];
+        if (!d.empty() && st.back() == ss * dd) {
+          d.back() *= dd;
+          st.back() = ss;
+        } else {
+          d.push_back(dd);
+          st.push_back(ss);
+        }
+      }
+      if (d.size() > 4) return false;
+      if (d.empty()) {
+        d.push_back(1);
+        st.push_back(0);
+      }
+      v.rank = (int)d.size();
+      for (int i = 0; i < v.rank; ++i) {
+        v.dims[i] = (int)d[i];
+        v.str[i] = st[i];
+      }
+      return true;
+    };
+    if (group_stride(oy, Ls) < 0 || !mk(oy, Kx, g.vbk) || !mk(oy, Ns, g.vbn))
+      throw Error(-1, "contract: planes consumer needs a gatherable right operand");
+    g.vam.rank = 1;
+    g.vam.dims[0] = (int)Msz;
+    g.vak.rank = 1;
+    g.vak.dims[0] = (int)Ksz;
+    g.B = Y.p;
+    g.conjB = cy;
+    g.nb1 = c.nb;
+    g.nb2 = (int)Lsz;
+    g.sb1 = Y.bstride;
+    g.sb2 = Ls.empty() ? 0 : group_stride(oy, Ls);
+    if (P.nz != g.nb1 * g.nb2) throw Error(-1, "contract: planes batch mismatch");
+    const std::string gout = Ls + Ms + Ns;
+    std::vector<int> gshape;
+    for (char ch : gout) gshape.push_back(dim[ch]);
+    Tensor C = new_tensor_n(c, gshape, c.nb);
+    g.C = C.p;
+    g.cm = Nsz;
+    g.sc1 = C.bstride;
+    g.sc2 = Msz * Nsz;
+    g.work_per_sample = Msz * Nsz * Ksz * Lsz;
+    g.m_per_sample = (int)Msz;
+    if (!gemm(c, g)) throw Error(-1, "contract: planes consumer not on the tensor cores");
+    if (gout == out) {
+      C.shape = oshape;
+      return C;
+    }
+    std::string dst(lout), src = gout;
+    for (char ch : dst)
+      if (src.find(ch) == std::string::npos) src.push_back(ch);
+    Tensor Ct = C;
+    Ct.shape.clear();
+    for (char ch : src) Ct.shape.push_back(dim.count(ch) ? dim[ch] : 1);
+    return permute(c, Ct, src.c_str(), dst.c_str(), false);
+  }
 
   // choose the K order: keep whichever operand's order avoids a permute, else the larger's
   std::string Kx = order_in(ox.lab, Ks), Ky = order_in(oy.lab, Ks);
@@ -660,12 +738,15 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
   Tensor C;
   std::vector<int> gshape;
   for (char ch : gout) gshape.push_back(dim[ch]);
-  if (direct) {
+  if (req) {
+    // no complex64 output: the epilogue writes the consumer's planes (allocated below)
+  } else if (direct) {
     C = new_tensor_n(c, oshape, per_out ? c.nb : 1);
   } else {
     C = new_tensor_n(c, gshape.empty() ? std::vector<int>{1} : gshape, per_out ? c.nb : 1);
   }
   if (!per_out) C.bstride = 0;
+  if (req) C.bstride = Msz * Nsz;  // the planes hold the samples back to back, like a dense C
 
   GemmDesc g;
   g.M = (int)Msz;
@@ -730,6 +811,95 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
     g.amaxC = C.mem->make_amax();
     g.amaxC_n = C.mem->tail_n;
   }
+  if (req) {
+    // ---- plane output (contract_planes): C goes straight into the consumer's A planes
+    if (!per_out || !Ls.empty() || g.nb1 != 1 || g.nb2 != 1 || Ms.empty() || Ns.empty())
+      throw Error(-1, "contract_planes: unsupported GEMM form");
+    const std::string &zl = req->zl, &rl = req->rl, &kl = req->kl;
+    if (zl.size() + rl.size() + kl.size() != out.size() || kl.empty() || rl.empty())
+      throw Error(-1, "contract_planes: the consumer labels must partition the output labels");
+    auto grp_of = [&](char ch) -> int {
+      if (zl.find(ch) != std::string::npos) return 0;
+      if (rl.find(ch) != std::string::npos) return 1;
+      if (kl.find(ch) != std::string::npos) return 2;
+      throw Error(-1, "contract_planes: output label missing from the consumer labels");
+    };
+    auto prod_of = [&](const std::string& l) {
+      int64_t r = 1;
+      for (char ch : l) r *= dim[ch];
+      return r;
+    };
+    auto stride_in = [&](const std::string& l, char ch) {
+      int64_t r = 1;
+      for (size_t i = l.find(ch) + 1; i < l.size(); ++i) r *= dim[l[i]];
+      return r;
+    };
+    const char inner = kl.back();
+    const int64_t NZ = prod_of(zl), Mc = prod_of(rl), Kc = prod_of(kl);
+    const int64_t Mpc = (Mc + 255) / 256 * 256, Krpc = (2 * Kc + 63) / 64 * 64;
+    if (dim[inner] != 128 || Ms.back() != inner || Mpc != Mc || Krpc != 2 * Kc || Mc <= 128)
+      throw Error(-1, "contract_planes: shapes do not allow plane output");
+    const int64_t nsb = Kc / 128;
+    auto digit = [&](char ch, int64_t& po, int64_t& so) {
+      const int gi = grp_of(ch);
+      if (gi == 0) {
+        const int64_t st = stride_in(zl, ch);
+        po = st * Mpc * Krpc;
+        so = st * nsb * Mpc;
+      } else if (gi == 1) {
+        const int64_t st = stride_in(rl, ch);
+        po = st * Krpc;
+        so = st;
+      } else {
+        const int64_t st = stride_in(kl, ch);
+        po = 2 * st;
+        so = (ch == inner) ? 0 : (st / 128) * Mpc;
+      }
+    };
+    PlaneOut pout;
+    const bool folded = (g.M == Msz * c.nb) && c.nb > 1;
+    if (!folded && c.nb != 1 && g.M != Msz) throw Error(-1, "contract_planes: batch not folded");
+    auto add = [](PView& v, int d, int64_t po, int64_t so) {
+      if (v.rank >= 4) throw Error(-1, "contract_planes: more than four digits");
+      v.dims[v.rank] = d;
+      v.po[v.rank] = po;
+      v.so[v.rank] = so;
+      ++v.rank;
+    };
+    if (folded) add(pout.vm, c.nb, NZ * Mpc * Krpc, NZ * nsb * Mpc);
+    for (char ch : Ms) {
+      int64_t po, so;
+      digit(ch, po, so);
+      add(pout.vm, dim[ch], po, so);
+    }
+    for (char ch : Ns) {
+      int64_t po, so;
+      digit(ch, po, so);
+      add(pout.vn, dim[ch], po, so);
+    }
+    auto P = std::make_shared<Planes>();
+    P->lab = zl + rl + kl;
+    P->nz = (int)(c.nb * NZ);
+    P->Mp = (int)Mpc;
+    P->Krp = (int)Krpc;
+    P->nsb = (int)nsb;
+    const size_t nh = (size_t)P->nz * Mpc * Krpc;
+    P->hi = std::make_shared<DevBuf>(nh * 2, c.stream);
+    P->lo = std::make_shared<DevBuf>(nh * 2, c.stream);
+    P->asc = std::make_shared<DevBuf>((size_t)P->nz * nsb * Mpc * sizeof(float), c.stream);
+    pout.hi = P->hi->as<__half>();
+    pout.lo = P->lo->as<__half>();
+    pout.asc = P->asc->as<float>();
+    g.po = &pout;
+    g.C = nullptr;
+    g.amaxC = nullptr;
+    if (!gemm(c, g)) throw Error(-1, "contract_planes: not on the tensor cores");
+    Tensor T;
+    T.planes = P;
+    for (char ch : P->lab) T.shape.push_back(dim[ch]);
+    T.bstride = T.size();
+    return T;
+  }
   const bool tc = gemm(c, g);
   if (!tc && C.mem) C.mem->drop_amax();
   if (direct) return C;
@@ -749,6 +919,17 @@ Tensor contract(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Te
     R.mem->make_amax();
   }
   return R;
+}
+
+Tensor contract(Ctx& c, const Tensor& A, const char* la, bool conjA, const Tensor& B, const char* lb, bool conjB,
+                const char* lout) {
+  return contract_impl(c, A, la, conjA, B, lb, conjB, lout, nullptr);
+}
+
+Tensor contract_planes(Ctx& c, const Tensor& A, const char* la, bool conjA, const Tensor& B, const char* lb,
+                       bool conjB, const char* lout, const char* zl, const char* rl, const char* kl) {
+  PlaneReq r{zl, rl, kl};
+  return contract_impl(c, A, la, conjA, B, lb, conjB, lout, &r);
 }
 
 }  // namespace tn

@@ -11,16 +11,28 @@
 #include <string>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "common.h"
 #include "prof.h"
 
 namespace tn {
+
+// FP16 hi/lo planes of a GEMM's A operand (K-major [z][Mp][Krp] halves, element (r, 2k + c)) and
+// their per-(row, SB_K block) scales [z][nsb][Mp] (1/s), written directly by the epilogue of the
+// GEMM that produces the operand (contract_planes) and consumed by contract() with no prep pass.
+struct Planes {
+  std::shared_ptr<DevBuf> hi, lo, asc;
+  std::string lab;  // logical labels of the operand: batch labels, row labels, K labels (outer -> inner)
+  int nz = 0, Mp = 0, Krp = 0, nsb = 0;
+};
 
 struct Tensor {
   std::shared_ptr<DevBuf> mem;
   float2* p = nullptr;
   std::vector<int> shape;
   int64_t bstride = 0;  // elements between consecutive samples; 0 = shared by all samples
+  std::shared_ptr<Planes> planes;  // set (and p null) for a tensor held only as GEMM A planes
   int64_t size() const { return prod(shape); }
   int rank() const { return (int)shape.size(); }
 };
@@ -57,6 +69,15 @@ void zero(Ctx& c, Tensor& t, int nb);
 Tensor contract(Ctx& c, const Tensor& A, const char* la, bool conjA, const Tensor& B,
                 const char* lb, bool conjB, const char* lout);
 
+// As contract(), but the result is written straight into the A-operand planes of the next
+// contraction instead of complex64 memory: zl / rl / kl are that contraction's batch, row and
+// K labels (a partition of lout's labels; kl's innermost label must be the innermost row label
+// of this GEMM, of dimension SB_K). The returned tensor (labels zl rl kl) can only be passed as
+// the first operand of contract() with exactly those labels. Tensor-core path only; throws
+// TN_E_ARG where the shapes do not allow it (callers check planes_ok first).
+Tensor contract_planes(Ctx& c, const Tensor& A, const char* la, bool conjA, const Tensor& B, const char* lb,
+                       bool conjB, const char* lout, const char* zl, const char* rl, const char* kl);
+
 // Reorder the axes: out labels are a permutation of in labels.
 Tensor permute(Ctx& c, const Tensor& A, const char* la, const char* lout, bool conj = false);
 
@@ -71,8 +92,26 @@ struct View4 {
 // C[m, n] (+)= sum_k A(m, k) B(k, n), A(m,k) = A[m*am + k*ak], B(k,n) = B[k*bk + n*bn].
 // When the v* views are set (rank > 0) they replace the single strides (tensor-core path
 // only): the operand preparation gathers straight from the multi-axis layout.
+// Plane output of a GEMM (contract_planes): element (m, n) of C goes to plane offset
+// po(m) + po(n) (halves) and its scale block to so(m) + so(n); each side decomposes its index
+// into up to four digits (outer -> inner) with a plane stride and a scale stride per digit.
+struct PView {
+  int rank = 0;
+  int dims[4] = {1, 1, 1, 1};
+  int64_t po[4] = {0, 0, 0, 0};
+  int64_t so[4] = {0, 0, 0, 0};
+};
+struct PlaneOut {
+  __half* hi = nullptr;
+  __half* lo = nullptr;
+  float* asc = nullptr;
+  PView vm, vn;
+};
+
 struct GemmDesc {
   View4 vam, vak, vbk, vbn;
+  const Planes* pa = nullptr;   // A given as planes (no prep)
+  const PlaneOut* po = nullptr; // C written as the next GEMM's A planes
   int M = 0, N = 0, K = 0;
   const float2* A = nullptr;
   int64_t am = 0, ak = 0;

@@ -302,6 +302,19 @@ int64_t per_sample_bytes(const Layout& L, int R, int chi) {
 // pa_log / pa_phase (optional, device [nb]): ln|a| and arg a of the amplitude carried along
 // the sampling path (m_{N_b-1 -> N_b} . X_{N_b}; p(x) = |a|^2 when the fits
 // are (near) exact): the n-fits' log-norms, the merge normalisations and the final scalar.
+// Whether a ladder GEMM (Y2 = Y1 . M_j or G2 = G1 . M_j) can write its closure's A planes
+// directly (contract_planes): rows = rbond x ebond (the closure's M, a whole number of CTA-pair
+// tiles), inner K = kbond = one scale block (128 complex), a down edge (d > 1), tensor-core GEMMs.
+// TN_LADDER_PLANES=0 disables it (A/B measurements).
+bool ladder_planes_ok(const Ctx& c, int rbond, int ebond, int d, int kbond) {
+  static const bool off = getenv("TN_LADDER_PLANES") && std::atoi(getenv("TN_LADDER_PLANES")) == 0;
+  if (off || c.gemm_mode == 1 || ebond <= 1 || d <= 1 || kbond != 128) return false;
+  const int64_t rows = (int64_t)rbond * ebond;
+  return rows % 256 == 0 && rows > 128 && ((int64_t)ebond * d) % 128 == 0 &&
+         tc_eligible(c, (int64_t)rbond * 2 * kbond, (int64_t)ebond * d, (int64_t)d * ebond,
+                     (int64_t)rbond * 2 * kbond * ebond * d * d * ebond);
+}
+
 void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double* u_dev, uint8_t* bits_dev,
                   double* logq_dev, double* cond_dev, uint32_t* flags_dev, double* pa_log = nullptr,
                   double* pa_phase = nullptr) {
@@ -353,10 +366,18 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
     Tensor Rr = ones(c, {1, 1, 1}, nb);
     for (int j = W - 1; j >= 0; --j) {
       Tensor Y1 = contract(c, n[j], "asdz", false, Rr, "zfZ", false, "asdfZ");
-      Tensor Y2;
-      if (ms.tops[j].p) Y2 = contract(c, Y1, "asdfZ", false, ms.tops[j], "edDf", false, "asZeD");
-      else Y2 = permute(c, Y1, "asdfZ", "asZfd");  // identity: e = f, d = D = 1
-      Rs[j] = contract(c, Y2, "asZeD", false, n[j], "AsDZ", true, "saeA");
+      if (ladder_planes_ok(c, n[j].shape[0], ms.tops[j].p ? ms.tops[j].shape[0] : 0, n[j].shape[2], n[j].shape[3])) {
+        // Y2 = Y1 . M_j written by its GEMM straight into the FP16 A planes of the closure
+        // Rs = Y2 . conj(n_j) (rows (a, e) per (sample, s), K = (D, Z)): no complex64 Y2 and no
+        // operand prep for the closure
+        Tensor Y2p = contract_planes(c, Y1, "asdfZ", false, ms.tops[j], "edDf", false, "asZeD", "s", "ae", "DZ");
+        Rs[j] = contract(c, Y2p, "saeDZ", false, n[j], "AsDZ", true, "saeA");
+      } else {
+        Tensor Y2;
+        if (ms.tops[j].p) Y2 = contract(c, Y1, "asdfZ", false, ms.tops[j], "edDf", false, "asZeD");
+        else Y2 = permute(c, Y1, "asdfZ", "asZfd");  // identity: e = f, d = D = 1
+        Rs[j] = contract(c, Y2, "asZeD", false, n[j], "AsDZ", true, "saeA");
+      }
       nan_check(c, ("Rs row " + std::to_string(b) + " j " + std::to_string(j)).c_str(), Rs[j], nb);
       if (j > 0) {
         Rr = sum2(c, Rs[j]);
@@ -375,10 +396,17 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
       proj[j] = nx;
       if (j + 1 < W) {
         Tensor G1 = contract(c, Lx, "aeA", false, nx, "adz", false, "eAdz");
-        Tensor G2;
-        if (ms.tops[j].p) G2 = contract(c, G1, "eAdz", false, ms.tops[j], "edDf", false, "AzDf");
-        else G2 = permute(c, G1, "eAdz", "Azde");  // identity: f = e, d = D = 1
-        Lx = contract(c, G2, "AzDf", false, nx, "ADZ", true, "zfZ");
+        if (ladder_planes_ok(c, nx.shape[2], ms.tops[j].p ? ms.tops[j].shape[3] : 0, nx.shape[1], nx.shape[0])) {
+          // G2 = G1 . M_j straight into the A planes of Lx = G2 . conj(n_j[x]) (rows (z, f),
+          // K = (D, A))
+          Tensor G2p = contract_planes(c, G1, "eAdz", false, ms.tops[j], "edDf", false, "zADf", "", "zf", "DA");
+          Lx = contract(c, G2p, "zfDA", false, nx, "ADZ", true, "zfZ");
+        } else {
+          Tensor G2;
+          if (ms.tops[j].p) G2 = contract(c, G1, "eAdz", false, ms.tops[j], "edDf", false, "AzDf");
+          else G2 = permute(c, G1, "eAdz", "Azde");  // identity: f = e, d = D = 1
+          Lx = contract(c, G2, "AzDf", false, nx, "ADZ", true, "zfZ");
+        }
         nan_check(c, ("Lx pre-norm row " + std::to_string(b) + " j " + std::to_string(j)).c_str(), Lx, nb);
         normalize(c, Lx, nb, nullptr, false);
         nan_check(c, ("Lx row " + std::to_string(b) + " j " + std::to_string(j)).c_str(), Lx, nb);
