@@ -87,6 +87,7 @@ struct TcParams {
   // per-(row, block) scales; a CTA's 128 rows are exactly one scale block of that operand
   int pout;
   PView pvm, pvn;
+  int64_t pzpo, pzso;
   __half* pho;
   __half* plo;
   float* psc;
@@ -708,6 +709,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         const float sB = mB > 0.f ? ldexpf(1.f, -scale_exp(mB)) : 1.f;
         int64_t pm, sm, pnA, snA, pnB, snB;
         pview_off(p.pvm, mrow, pm, sm);
+        pm += (int64_t)(p.z0 + tl.z) * p.pzpo;
+        sm += (int64_t)(p.z0 + tl.z) * p.pzso;
         pview_off(p.pvn, n0 + lane, pnA, snA);
         pview_off(p.pvn, n0 + lane + 32, pnB, snB);
         if (lg == 0) {  // one writer per block: sm is the same for the CTA's 128 rows
@@ -2107,7 +2110,7 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       throw Error(-1, "gemm: A planes do not match the GEMM");
     zc = nbz;
   }
-  if (g.po && (ksplit != 1 || g.M % (2 * TC_BM) != 0 || g.N % 128 != 0 || nbz != 1))
+  if (g.po && (ksplit != 1 || g.M % (2 * TC_BM) != 0 || g.N % 128 != 0 || g.nb2 != 1 || (g.pa == nullptr && zc < nbz)))
     throw Error(-1, "gemm: plane output needs whole tiles and no split-K");
   DevBuf ah(g.pa ? 0 : (size_t)zc * per_z * 2, c.stream), al(g.pa ? 0 : (size_t)zc * per_z * 2, c.stream);
   DevBuf asc(g.pa ? 0 : (size_t)zc * nsb * Mp * sizeof(float), c.stream);
@@ -2179,6 +2182,8 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
       p.pout = 1;
       p.pvm = g.po->vm;
       p.pvn = g.po->vn;
+      p.pzpo = g.po->zpo;
+      p.pzso = g.po->zso;
       p.pho = g.po->hi;
       p.plo = g.po->lo;
       p.psc = g.po->asc;

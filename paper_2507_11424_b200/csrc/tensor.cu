@@ -518,6 +518,105 @@ struct PlaneReq {
   std::string zl, rl, kl;
 };
 
+// The plane-output half of contract_planes: map every output digit of the GEMM g (M digits:
+// the folded sample, then Ms; N digits: Ns) to the consumer's planes, allocate them and run g.
+static Tensor plane_output(Ctx& c, GemmDesc& g, const PlaneReq& rq, std::map<char, int>& dim,
+                           const std::string& Ls, const std::string& Ms, const std::string& Ns,
+                           const std::string& out, bool per_out, int64_t Msz) {
+    const PlaneReq* req = &rq;
+    // ---- plane output (contract_planes): C goes straight into the consumer's A planes
+    if (!per_out || !Ls.empty() || g.nb2 != 1 || (g.nb1 != 1 && g.nb1 != c.nb) || Ms.empty() || Ns.empty())
+      throw Error(-1, "contract_planes: unsupported GEMM form");
+    const std::string &zl = req->zl, &rl = req->rl, &kl = req->kl;
+    if (zl.size() + rl.size() + kl.size() != out.size() || kl.empty() || rl.empty())
+      throw Error(-1, "contract_planes: the consumer labels must partition the output labels");
+    auto grp_of = [&](char ch) -> int {
+      if (zl.find(ch) != std::string::npos) return 0;
+      if (rl.find(ch) != std::string::npos) return 1;
+      if (kl.find(ch) != std::string::npos) return 2;
+      throw Error(-1, "contract_planes: output label missing from the consumer labels");
+    };
+    auto prod_of = [&](const std::string& l) {
+      int64_t r = 1;
+      for (char ch : l) r *= dim[ch];
+      return r;
+    };
+    auto stride_in = [&](const std::string& l, char ch) {
+      int64_t r = 1;
+      for (size_t i = l.find(ch) + 1; i < l.size(); ++i) r *= dim[l[i]];
+      return r;
+    };
+    const char inner = kl.back();
+    const int64_t NZ = prod_of(zl), Mc = prod_of(rl), Kc = prod_of(kl);
+    const int64_t Mpc = (Mc + 255) / 256 * 256, Krpc = (2 * Kc + 63) / 64 * 64;
+    if (dim[inner] != 128 || Ms.back() != inner || Mpc != Mc || Krpc != 2 * Kc || Mc <= 128)
+      throw Error(-1, "contract_planes: shapes do not allow plane output");
+    const int64_t nsb = Kc / 128;
+    auto digit = [&](char ch, int64_t& po, int64_t& so) {
+      const int gi = grp_of(ch);
+      if (gi == 0) {
+        const int64_t st = stride_in(zl, ch);
+        po = st * Mpc * Krpc;
+        so = st * nsb * Mpc;
+      } else if (gi == 1) {
+        const int64_t st = stride_in(rl, ch);
+        po = st * Krpc;
+        so = st;
+      } else {
+        const int64_t st = stride_in(kl, ch);
+        po = 2 * st;
+        so = (ch == inner) ? 0 : (st / 128) * Mpc;
+      }
+    };
+    PlaneOut pout;
+    const bool folded = (g.M == Msz * c.nb) && c.nb > 1;
+    if (!folded && g.M != Msz) throw Error(-1, "contract_planes: unexpected GEMM rows");
+    auto add = [](PView& v, int d, int64_t po, int64_t so) {
+      if (v.rank >= 4) throw Error(-1, "contract_planes: more than four digits");
+      v.dims[v.rank] = d;
+      v.po[v.rank] = po;
+      v.so[v.rank] = so;
+      ++v.rank;
+    };
+    if (folded) add(pout.vm, c.nb, NZ * Mpc * Krpc, NZ * nsb * Mpc);
+    else if (g.nb1 > 1) {  // samples on the GEMM's batch index
+      pout.zpo = NZ * Mpc * Krpc;
+      pout.zso = NZ * nsb * Mpc;
+    }
+    for (char ch : Ms) {
+      int64_t po, so;
+      digit(ch, po, so);
+      add(pout.vm, dim[ch], po, so);
+    }
+    for (char ch : Ns) {
+      int64_t po, so;
+      digit(ch, po, so);
+      add(pout.vn, dim[ch], po, so);
+    }
+    auto P = std::make_shared<Planes>();
+    P->lab = zl + rl + kl;
+    P->nz = (int)(c.nb * NZ);
+    P->Mp = (int)Mpc;
+    P->Krp = (int)Krpc;
+    P->nsb = (int)nsb;
+    const size_t nh = (size_t)P->nz * Mpc * Krpc;
+    P->hi = std::make_shared<DevBuf>(nh * 2, c.stream);
+    P->lo = std::make_shared<DevBuf>(nh * 2, c.stream);
+    P->asc = std::make_shared<DevBuf>((size_t)P->nz * nsb * Mpc * sizeof(float), c.stream);
+    pout.hi = P->hi->as<__half>();
+    pout.lo = P->lo->as<__half>();
+    pout.asc = P->asc->as<float>();
+    g.po = &pout;
+    g.C = nullptr;
+    g.amaxC = nullptr;
+    if (!gemm(c, g)) throw Error(-1, "contract_planes: not on the tensor cores");
+    Tensor T;
+    T.planes = P;
+    for (char ch : P->lab) T.shape.push_back(dim[ch]);
+    T.bstride = T.size();
+    return T;
+}
+
 static Tensor contract_impl(Ctx& c, const Tensor& A0, const char* la0, bool conjA0, const Tensor& B0,
                             const char* lb0, bool conjB0, const char* lout, const PlaneReq* req) {
   // dims of every label
@@ -627,6 +726,9 @@ static Tensor contract_impl(Ctx& c, const Tensor& A0, const char* la0, bool conj
     g.sb1 = Y.bstride;
     g.sb2 = Ls.empty() ? 0 : group_stride(oy, Ls);
     if (P.nz != g.nb1 * g.nb2) throw Error(-1, "contract: planes batch mismatch");
+    g.work_per_sample = Msz * Nsz * Ksz * Lsz;
+    g.m_per_sample = (int)Msz;
+    if (req) return plane_output(c, g, *req, dim, Ls, Ms, Ns, out, per_out, Msz);  // planes in and out
     const std::string gout = Ls + Ms + Ns;
     std::vector<int> gshape;
     for (char ch : gout) gshape.push_back(dim[ch]);
@@ -811,95 +913,7 @@ static Tensor contract_impl(Ctx& c, const Tensor& A0, const char* la0, bool conj
     g.amaxC = C.mem->make_amax();
     g.amaxC_n = C.mem->tail_n;
   }
-  if (req) {
-    // ---- plane output (contract_planes): C goes straight into the consumer's A planes
-    if (!per_out || !Ls.empty() || g.nb1 != 1 || g.nb2 != 1 || Ms.empty() || Ns.empty())
-      throw Error(-1, "contract_planes: unsupported GEMM form");
-    const std::string &zl = req->zl, &rl = req->rl, &kl = req->kl;
-    if (zl.size() + rl.size() + kl.size() != out.size() || kl.empty() || rl.empty())
-      throw Error(-1, "contract_planes: the consumer labels must partition the output labels");
-    auto grp_of = [&](char ch) -> int {
-      if (zl.find(ch) != std::string::npos) return 0;
-      if (rl.find(ch) != std::string::npos) return 1;
-      if (kl.find(ch) != std::string::npos) return 2;
-      throw Error(-1, "contract_planes: output label missing from the consumer labels");
-    };
-    auto prod_of = [&](const std::string& l) {
-      int64_t r = 1;
-      for (char ch : l) r *= dim[ch];
-      return r;
-    };
-    auto stride_in = [&](const std::string& l, char ch) {
-      int64_t r = 1;
-      for (size_t i = l.find(ch) + 1; i < l.size(); ++i) r *= dim[l[i]];
-      return r;
-    };
-    const char inner = kl.back();
-    const int64_t NZ = prod_of(zl), Mc = prod_of(rl), Kc = prod_of(kl);
-    const int64_t Mpc = (Mc + 255) / 256 * 256, Krpc = (2 * Kc + 63) / 64 * 64;
-    if (dim[inner] != 128 || Ms.back() != inner || Mpc != Mc || Krpc != 2 * Kc || Mc <= 128)
-      throw Error(-1, "contract_planes: shapes do not allow plane output");
-    const int64_t nsb = Kc / 128;
-    auto digit = [&](char ch, int64_t& po, int64_t& so) {
-      const int gi = grp_of(ch);
-      if (gi == 0) {
-        const int64_t st = stride_in(zl, ch);
-        po = st * Mpc * Krpc;
-        so = st * nsb * Mpc;
-      } else if (gi == 1) {
-        const int64_t st = stride_in(rl, ch);
-        po = st * Krpc;
-        so = st;
-      } else {
-        const int64_t st = stride_in(kl, ch);
-        po = 2 * st;
-        so = (ch == inner) ? 0 : (st / 128) * Mpc;
-      }
-    };
-    PlaneOut pout;
-    const bool folded = (g.M == Msz * c.nb) && c.nb > 1;
-    if (!folded && c.nb != 1 && g.M != Msz) throw Error(-1, "contract_planes: batch not folded");
-    auto add = [](PView& v, int d, int64_t po, int64_t so) {
-      if (v.rank >= 4) throw Error(-1, "contract_planes: more than four digits");
-      v.dims[v.rank] = d;
-      v.po[v.rank] = po;
-      v.so[v.rank] = so;
-      ++v.rank;
-    };
-    if (folded) add(pout.vm, c.nb, NZ * Mpc * Krpc, NZ * nsb * Mpc);
-    for (char ch : Ms) {
-      int64_t po, so;
-      digit(ch, po, so);
-      add(pout.vm, dim[ch], po, so);
-    }
-    for (char ch : Ns) {
-      int64_t po, so;
-      digit(ch, po, so);
-      add(pout.vn, dim[ch], po, so);
-    }
-    auto P = std::make_shared<Planes>();
-    P->lab = zl + rl + kl;
-    P->nz = (int)(c.nb * NZ);
-    P->Mp = (int)Mpc;
-    P->Krp = (int)Krpc;
-    P->nsb = (int)nsb;
-    const size_t nh = (size_t)P->nz * Mpc * Krpc;
-    P->hi = std::make_shared<DevBuf>(nh * 2, c.stream);
-    P->lo = std::make_shared<DevBuf>(nh * 2, c.stream);
-    P->asc = std::make_shared<DevBuf>((size_t)P->nz * nsb * Mpc * sizeof(float), c.stream);
-    pout.hi = P->hi->as<__half>();
-    pout.lo = P->lo->as<__half>();
-    pout.asc = P->asc->as<float>();
-    g.po = &pout;
-    g.C = nullptr;
-    g.amaxC = nullptr;
-    if (!gemm(c, g)) throw Error(-1, "contract_planes: not on the tensor cores");
-    Tensor T;
-    T.planes = P;
-    for (char ch : P->lab) T.shape.push_back(dim[ch]);
-    T.bstride = T.size();
-    return T;
-  }
+  if (req) return plane_output(c, g, *req, dim, Ls, Ms, Ns, out, per_out, Msz);
   const bool tc = gemm(c, g);
   if (!tc && C.mem) C.mem->drop_amax();
   if (direct) return C;

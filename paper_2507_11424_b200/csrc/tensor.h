@@ -106,6 +106,7 @@ struct PlaneOut {
   __half* lo = nullptr;
   float* asc = nullptr;
   PView vm, vn;
+  int64_t zpo = 0, zso = 0;  // plane / scale stride of the GEMM's batch index (unfolded samples)
 };
 
 struct GemmDesc {

@@ -305,7 +305,7 @@ int64_t per_sample_bytes(const Layout& L, int R, int chi) {
 // Whether a ladder GEMM (Y2 = Y1 . M_j or G2 = G1 . M_j) can write its closure's A planes
 // directly (contract_planes): rows = rbond x ebond (the closure's M, a whole number of CTA-pair
 // tiles), inner K = kbond = one scale block (128 complex), a down edge (d > 1), tensor-core GEMMs.
-// TN_LADDER_PLANES=0 disables it (A/B measurements).
+// TN_LADDER_PLANES=0 disables it, =1 keeps only the G2 / Y2 planes (A/B measurements).
 bool ladder_planes_ok(const Ctx& c, int rbond, int ebond, int d, int kbond) {
   static const bool off = getenv("TN_LADDER_PLANES") && std::atoi(getenv("TN_LADDER_PLANES")) == 0;
   if (off || c.gemm_mode == 1 || ebond <= 1 || d <= 1 || kbond != 128) return false;
@@ -313,6 +313,15 @@ bool ladder_planes_ok(const Ctx& c, int rbond, int ebond, int d, int kbond) {
   return rows % 256 == 0 && rows > 128 && ((int64_t)ebond * d) % 128 == 0 &&
          tc_eligible(c, (int64_t)rbond * 2 * kbond, (int64_t)ebond * d, (int64_t)d * ebond,
                      (int64_t)rbond * 2 * kbond * ebond * d * d * ebond);
+}
+
+// Whether G1 = Lx . n_j[x] (M = (A, e), N = (d, z), K = a) can write G2's A planes (rows (z, A),
+// K = (d, e)): e is one scale block, whole CTA-pair tiles, a down edge.
+bool g1_planes_ok(const Ctx& c, int e, int A, int d, int z) {
+  static const bool off = getenv("TN_LADDER_PLANES") && std::atoi(getenv("TN_LADDER_PLANES")) < 2;
+  if (off || c.gemm_mode == 1 || e != 128 || d <= 1 || A <= 1) return false;
+  const int64_t rows = (int64_t)z * A;
+  return rows % 256 == 0 && ((int64_t)A * e) % 256 == 0 && ((int64_t)d * z) % 128 == 0;
 }
 
 void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double* u_dev, uint8_t* bits_dev,
@@ -395,13 +404,23 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
       Tensor nx = select_s(c, n[j], xbuf.as<int>(), nb);
       proj[j] = nx;
       if (j + 1 < W) {
-        Tensor G1 = contract(c, Lx, "aeA", false, nx, "adz", false, "eAdz");
-        if (ladder_planes_ok(c, nx.shape[2], ms.tops[j].p ? ms.tops[j].shape[3] : 0, nx.shape[1], nx.shape[0])) {
+        if (ladder_planes_ok(c, nx.shape[2], ms.tops[j].p ? ms.tops[j].shape[3] : 0, nx.shape[1], nx.shape[0]) &&
+            g1_planes_ok(c, Lx.shape[1], Lx.shape[2], nx.shape[1], nx.shape[2])) {
+          // G1 = Lx . n_j[x] into the A planes of G2 (rows (z, A), K = (d, e)), G2 = G1 . M_j
+          // into the A planes of Lx = G2 . conj(n_j[x]) (rows (z, f), K = (D, A)): neither
+          // intermediate exists in complex64 and neither GEMM preps its A operand
+          Tensor G1p = contract_planes(c, Lx, "aeA", false, nx, "adz", false, "Aedz", "", "zA", "de");
+          Tensor G2p = contract_planes(c, G1p, "zAde", false, ms.tops[j], "edDf", false, "zADf", "", "zf", "DA");
+          Lx = contract(c, G2p, "zfDA", false, nx, "ADZ", true, "zfZ");
+        } else if (ladder_planes_ok(c, nx.shape[2], ms.tops[j].p ? ms.tops[j].shape[3] : 0, nx.shape[1],
+                                    nx.shape[0])) {
           // G2 = G1 . M_j straight into the A planes of Lx = G2 . conj(n_j[x]) (rows (z, f),
           // K = (D, A))
+          Tensor G1 = contract(c, Lx, "aeA", false, nx, "adz", false, "eAdz");
           Tensor G2p = contract_planes(c, G1, "eAdz", false, ms.tops[j], "edDf", false, "zADf", "", "zf", "DA");
           Lx = contract(c, G2p, "zfDA", false, nx, "ADZ", true, "zfZ");
         } else {
+          Tensor G1 = contract(c, Lx, "aeA", false, nx, "adz", false, "eAdz");
           Tensor G2;
           if (ms.tops[j].p) G2 = contract(c, G1, "eAdz", false, ms.tops[j], "edDf", false, "AzDf");
           else G2 = permute(c, G1, "eAdz", "Azde");  // identity: f = e, d = D = 1
