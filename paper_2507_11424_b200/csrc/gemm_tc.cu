@@ -652,16 +652,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
       for (int i = 0; i < 128; ++i) acc[i] = 0.f;
       const int nchunks = (tl.nkb + SB_KB - 1) / SB_KB;
-      const float* ascr = p.ascale + ((int64_t)tl.z * p.nsb + tl.kb0 / SB_KB) * p.Mp + row;  // row < Mp
-      const float* bscr = p.bscale + ((int64_t)(p.b_batched ? tl.z : 0) * p.nsb + tl.kb0 / SB_KB) * p.Np +
-                          ((tl.nblk * TC_BN + half * 128) >> 1);
+      // scale indices as 32-bit element offsets (the scale arrays hold < 2^32 floats; fewer
+      // live registers next to the 128 accumulators)
+      uint32_t ai = (uint32_t)((tl.z * p.nsb + tl.kb0 / SB_KB) * p.Mp + row);  // row < Mp
+      uint32_t bi = (uint32_t)(((p.b_batched ? tl.z : 0) * p.nsb + tl.kb0 / SB_KB) * p.Np +
+                               ((tl.nblk * TC_BN + half * 128) >> 1) + lane);
       float* fcol = epi_colsc + (warp - 2) * 64;  // this warp's 64 column factors of the chunk
-      for (int cc0 = 0; cc0 < nchunks; ++cc0, ++c) {
+      for (int cc0 = 0; cc0 < nchunks; ++cc0, ++c, ai += p.Mp, bi += p.Np) {
         const int buf = c & 1;
-        const float f = ascr[(int64_t)cc0 * p.Mp];  // 1/s of this row's scale block
+        const float f = p.ascale[ai];  // 1/s of this row's scale block
         __syncwarp();
-        fcol[lane] = bscr[(int64_t)cc0 * p.Np + lane];  // columns < Np
-        fcol[lane + 32] = bscr[(int64_t)cc0 * p.Np + lane + 32];
+        fcol[lane] = p.bscale[bi];  // columns < Np
+        fcol[lane + 32] = p.bscale[bi + 32];
         __syncwarp();
         mbar_wait(&acc_full[buf], (c >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -719,10 +721,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         }
         __half2* hi = reinterpret_cast<__half2*>(p.pho);
         __half2* lo = reinterpret_cast<__half2*>(p.plo);
+        // the innermost N digit runs over >= 32 aligned columns: a column's plane offset is that
+        // of the first column of its 32-group plus a multiple of the digit's stride
+        const bool lin = p.pvn.dims[p.pvn.rank - 1] % 32 == 0;
+        const int64_t pst = p.pvn.po[p.pvn.rank - 1];
+        const int64_t pg0 = __shfl_sync(0xffffffffu, pnA, 0), pg1 = __shfl_sync(0xffffffffu, pnB, 0);
 #pragma unroll
         for (int q = 0; q < 64; ++q) {
           const float sc = __shfl_sync(0xffffffffu, q < 32 ? sA : sB, q & 31);
-          const int64_t pn = __shfl_sync(0xffffffffu, q < 32 ? pnA : pnB, q & 31);
+          const int64_t pn = lin ? (q < 32 ? pg0 : pg1) + (q & 31) * pst
+                                 : __shfl_sync(0xffffffffu, q < 32 ? pnA : pnB, q & 31);
           __half2 h, l;
           split16x2(acc[2 * q] * sc, acc[2 * q + 1] * sc, h, l);
           const int64_t off = (pm + pn) >> 1;  // half2 index (complex element)
