@@ -520,6 +520,8 @@ struct PlaneReq {
 
 // The plane-output half of contract_planes: map every output digit of the GEMM g (M digits:
 // the folded sample, then Ms; N digits: Ns) to the consumer's planes, allocate them and run g.
+thread_local int64_t g_plane_gemms = 0;  // GEMMs run with plane output (tn_debug_plane_gemms)
+
 static Tensor plane_output(Ctx& c, GemmDesc& g, const PlaneReq& rq, std::map<char, int>& dim,
                            const std::string& Ls, const std::string& Ms, const std::string& Ns,
                            const std::string& out, bool per_out, int64_t Msz) {
@@ -610,6 +612,7 @@ static Tensor plane_output(Ctx& c, GemmDesc& g, const PlaneReq& rq, std::map<cha
     g.C = nullptr;
     g.amaxC = nullptr;
     if (!gemm(c, g)) throw Error(-1, "contract_planes: not on the tensor cores");
+    ++g_plane_gemms;
     Tensor T;
     T.planes = P;
     for (char ch : P->lab) T.shape.push_back(dim[ch]);
@@ -947,6 +950,13 @@ Tensor contract_planes(Ctx& c, const Tensor& A, const char* la, bool conjA, cons
 }
 
 }  // namespace tn
+
+// Test-only: GEMMs that wrote their consumer's planes since the last reset (this thread).
+extern "C" int64_t tn_debug_plane_gemms(int reset) {
+  const int64_t n = tn::g_plane_gemms;
+  if (reset) tn::g_plane_gemms = 0;
+  return n;
+}
 
 extern "C" int tn_debug_simt_log(void) {
   std::vector<std::pair<double, std::string>> rows;

@@ -159,6 +159,37 @@ def test_branch_superposition_metric_shapes_exact():
         assert abs(logq[k] - sum(math.log(r) for r in ref)) <= 1e-4 * max(1, abs(logq[k]))
 
 
+def test_metric_shapes_batch_composition_bitwise():
+    """The metric-shape ladder runs through the plane-output GEMMs (the ladder GEMMs write their
+    closures' FP16 A planes and block scales from the epilogue; G1 -> G2 -> Lx chained, the
+    samples on the GEMM batch index or folded into M): one batch of 4, batches of 1 and 3, and
+    the same samples in another order give bitwise the same bits, ln q and conditionals per
+    sample (results depend only on a sample's own uniforms). A state with
+    every vertex at full bonds (Vidal-like) on three full-width Willow rows, chi = 32,
+    chi_env = 128."""
+    lat = L.row_strip(L.willow105(), 1, 4)
+    st = S.vidal_like(lat, 32, seed=7, xi=8.0)
+    u = S.uniforms(4, lat.n, 31)
+    g = TNState(st)
+    import ctypes
+    from paper_2507_11424_b200 import _lib
+    _lib.lib().tn_debug_plane_gemms.restype = ctypes.c_int64
+    _lib.lib().tn_debug_plane_gemms(1)
+    ref = g.sample(lat.rows, 128, u, want_cond=True)
+    assert _lib.lib().tn_debug_plane_gemms(1) > 0  # the plane-output path ran
+    for mb in (1, 3):
+        g.set_option("max_batch", mb)
+        got = g.sample(lat.rows, 128, u, want_cond=True)
+        for a, b in zip(ref, got):
+            assert np.array_equal(a, b), mb
+    g.set_option("max_batch", 0)
+    perm = [2, 0, 3, 1]
+    got = g.sample(lat.rows, 128, u[perm], want_cond=True)
+    for a, b in zip(ref, got):
+        assert np.array_equal(a[perm], b)
+    assert np.isfinite(ref[1]).all()
+
+
 def test_ghz_eagle():
     lat = L.eagle127()
     st = S.ghz(lat, chi=2)
