@@ -411,7 +411,21 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
   }
   std::vector<int> D = fit_bonds(s, R);
   std::vector<Tensor> o(K);
-  for (int k = 0; k < K; ++k) {
+  // the shared initial guess of a single-layer fit, right-orthonormalised, from the state's
+  // cache when an earlier batch already built it (bitwise the same tensors)
+  std::string gkey;
+  bool guess_done = false;
+  if (!s.dbl && c.guess_cache) {
+    gkey = std::to_string(seed) + "/" + std::to_string(tag) + "/" + std::to_string(b1);
+    for (int k = 0; k < K; ++k)
+      for (int d : o_shape(s, cols[k], D[k], D[k + 1])) gkey += "," + std::to_string(d);
+    auto it = c.guess_cache->find(gkey);
+    if (it != c.guess_cache->end()) {
+      o = it->second;
+      guess_done = true;
+    }
+  }
+  for (int k = 0; k < K && !guess_done; ++k) {
     // the initial guess does not depend on the sample (R4: the hash key is (seed, tag, b,
     // k, i)): one shared copy, right-orthonormalised once for the whole batch below
     o[k] = new_tensor_n(c, o_shape(s, cols[k], D[k], D[k + 1]), 1);
@@ -419,7 +433,7 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
     hash_init(c, o[k], 1, seed, tag, b1, k);
   }
   // right-orthonormalise as a true gauge transformation (absorb the factor to the left)
-  for (int k = K - 1; k >= 1; --k) {
+  for (int k = K - 1; k >= 1 && !guess_done; --k) {
     Tensor C;
     Tensor q = right_orth(c, o[k], nb, &C);
     o[k] = q;
@@ -429,6 +443,10 @@ FitResult fit(Ctx& c, const DStrip& s, int R, int tag, int b1, uint64_t seed, in
     Tensor pv = view(prev, sh2);
     Tensor np = contract(c, pv, "aq", false, C, "bq", true, "ab");
     o[k - 1] = view(np, prev.shape);
+  }
+  if (!gkey.empty() && !guess_done) {
+    (*c.guess_cache)[gkey] = o;  // read-only from here on: the sweeps replace every site
+    TN_CUDA(cudaStreamSynchronize(c.stream));  // later batches may run on other streams
   }
   auto env_left = [&](const Env& Lk, int k) {
     Env L = rescaled(ops.absorb_left(Lk.t, cols[k], &o[k]), Lk);

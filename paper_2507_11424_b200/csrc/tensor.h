@@ -7,6 +7,7 @@
 // operands is folded into the GEMM M dimension when the other operand is shared across
 // samples (A_v, the norm environment M), so one launch covers the whole batch.
 #pragma once
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -56,6 +57,10 @@ struct Ctx {
   // norm-environment precompute; the double-layer fits split their chunk loops across them.
   void* comm = nullptr;
   int rank = 0, world = 1;
+  // The single-layer fits' right-orthonormalised initial guesses, by (seed, tag, row, output
+  // shapes): they do not depend on the samples (R4), so every sampling step after the first
+  // reuses them (owned by the state; see fit.cu).
+  std::shared_ptr<std::map<std::string, std::vector<Tensor>>> guess_cache;
 };
 
 // Allocate a tensor: per-sample (nb copies) when per_sample, else shared.

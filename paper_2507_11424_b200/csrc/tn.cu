@@ -771,6 +771,7 @@ int tn_load_state(const tn_graph* g, const double* const* tensors, int32_t chi, 
     }
     TN_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
     st->ctx.stream = st->stream;
+    st->ctx.guess_cache = std::make_shared<std::map<std::string, std::vector<Tensor>>>();
     if (const char* gm = getenv("TN_GEMM")) st->ctx.gemm_mode = std::atoi(gm);  // debugging override
     *out = st.release();
   });
@@ -814,6 +815,13 @@ int tn_free_state(tn_state* st) {
     cudaStreamSynchronize(st->stream);
     if (st->ctx.comm) ncclCommDestroy(reinterpret_cast<ncclComm_t>(st->ctx.comm));
     st->layouts.clear();
+    if (st->ctx.guess_cache) {  // built on whatever stream sampled first: free on the state's own
+      cudaDeviceSynchronize();
+      for (auto& kv : *st->ctx.guess_cache)
+        for (auto& t : kv.second)
+          if (t.mem) t.mem->s = st->stream;
+      st->ctx.guess_cache->clear();
+    }
     cudaStreamSynchronize(st->stream);
     cudaStreamDestroy(st->stream);
     delete st;
