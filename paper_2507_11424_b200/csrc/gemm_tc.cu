@@ -88,6 +88,7 @@ struct TcParams {
   int pout;
   PView pvm, pvn;
   int64_t pzpo, pzso;
+  int pmode;  // 1: scale block = a tile column of 128 rows; 2: a warp's 32 rows x 4 columns
   __half* pho;
   __half* plo;
   float* psc;
@@ -685,6 +686,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(acc_empty0 + (uint32_t)(buf * sizeof(uint64_t)));
+      }
+      if (POUT && p.pmode == 2) {
+        // Plane output, blocks of a warp's 32 rows x 4 adjacent columns (16 per warp): group
+        // maxima by four halving exchanges (8 + 4 + 2 + 1 shuffles: lane l holds group l / 2)
+        // and one more across the lane pair; no shared memory.
+        const int n0 = (tl.nblk * TC_BN + half * 128) >> 1;
+        const int64_t mrow = (int64_t)(tl.mblk0 + (int)rank) * 128 + lg * 32 + lane;
+        float g8[8];
+        const bool b16 = lane & 16;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float lo4 = 0.f, hi4 = 0.f;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int qa = 4 * j + t, qb = 4 * (j + 8) + t;
+            lo4 = fmaxf(lo4, fmaxf(fabsf(acc[2 * qa]), fabsf(acc[2 * qa + 1])));
+            hi4 = fmaxf(hi4, fmaxf(fabsf(acc[2 * qb]), fabsf(acc[2 * qb + 1])));
+          }
+          g8[j] = fmaxf(b16 ? hi4 : lo4, __shfl_xor_sync(0xffffffffu, b16 ? lo4 : hi4, 16));
+        }
+        float g4[4], g2[2];
+        const bool b8 = lane & 8, b4 = lane & 4, b2 = lane & 2;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          g4[j] = fmaxf(b8 ? g8[j + 4] : g8[j], __shfl_xor_sync(0xffffffffu, b8 ? g8[j] : g8[j + 4], 8));
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          g2[j] = fmaxf(b4 ? g4[j + 2] : g4[j], __shfl_xor_sync(0xffffffffu, b4 ? g4[j] : g4[j + 2], 4));
+        float g1 = fmaxf(b2 ? g2[1] : g2[0], __shfl_xor_sync(0xffffffffu, b2 ? g2[0] : g2[1], 2));
+        g1 = fmaxf(g1, __shfl_xor_sync(0xffffffffu, g1, 1));
+        const float sg = g1 > 0.f ? ldexpf(1.f, -scale_exp(g1)) : 1.f;
+        int64_t pm, sm, pnA, snA, pnB, snB;
+        pview_off(p.pvm, mrow, pm, sm);
+        pm += (int64_t)(p.z0 + tl.z) * p.pzpo;
+        sm += (int64_t)(p.z0 + tl.z) * p.pzso;
+        pview_off(p.pvn, n0 + lane, pnA, snA);
+        pview_off(p.pvn, n0 + lane + 32, pnB, snB);
+        if ((lane & 1) == 0) {  // group lane / 2: columns n0 + 4 (lane / 2) .. + 3 (sm: same for the warp)
+          int64_t pq, sq;
+          pview_off(p.pvn, n0 + 2 * lane, pq, sq);
+          p.psc[sm + sq] = g1 > 0.f ? inv_scale(g1) : 1.f;
+        }
+        __half2* hi = reinterpret_cast<__half2*>(p.pho);
+        __half2* lo = reinterpret_cast<__half2*>(p.plo);
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          const float sc = __shfl_sync(0xffffffffu, sg, (q >> 2) << 1);
+          const int64_t pn = __shfl_sync(0xffffffffu, q < 32 ? pnA : pnB, q & 31);
+          __half2 h, l;
+          split16x2(acc[2 * q] * sc, acc[2 * q + 1] * sc, h, l);
+          const int64_t off = (pm + pn) >> 1;  // half2 index: the warp's 32 rows are 32 adjacent k
+          hi[off] = h;
+          lo[off] = l;
+        }
+        continue;
       }
       if (POUT) {
         // Plane output: the CTA's 128 rows x this half's 64 complex columns; column q of the
@@ -2186,12 +2242,14 @@ bool gemm_tc(Ctx& c, const GemmDesc& g) {
     p.ascale = pasc;
     p.nsb = nsb;
     p.pout = 0;
+    p.pmode = 0;
     if (g.po) {
       p.pout = 1;
       p.pvm = g.po->vm;
       p.pvn = g.po->vn;
       p.pzpo = g.po->zpo;
       p.pzso = g.po->zso;
+      p.pmode = g.po->mode;
       p.pho = g.po->hi;
       p.plo = g.po->lo;
       p.psc = g.po->asc;

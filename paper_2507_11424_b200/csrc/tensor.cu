@@ -551,7 +551,19 @@ static Tensor plane_output(Ctx& c, GemmDesc& g, const PlaneReq& rq, std::map<cha
     const char inner = kl.back();
     const int64_t NZ = prod_of(zl), Mc = prod_of(rl), Kc = prod_of(kl);
     const int64_t Mpc = (Mc + 255) / 256 * 256, Krpc = (2 * Kc + 63) / 64 * 64;
-    if (dim[inner] != 128 || Ms.back() != inner || Mpc != Mc || Krpc != 2 * Kc || Mc <= 128)
+    // Scale-block shape in the producer's tile. Mode 1: the consumer's inner K label (128) is
+    // this GEMM's inner row digit -- a block is one column of a CTA's 128 rows. Mode 2: the
+    // inner K label (32) is the inner row digit and the next K label, this GEMM's inner column
+    // digit, supplies 4 -- a block is a warp's 32 rows x 4 adjacent columns.
+    int mode = 0;
+    char outer = 0;
+    if (dim[inner] == 128 && Ms.back() == inner) mode = 1;
+    else if (dim[inner] == 32 && Ms.back() == inner && kl.size() >= 2 && Ns.back() == kl[kl.size() - 2] &&
+             dim[kl[kl.size() - 2]] % 4 == 0) {
+      mode = 2;
+      outer = kl[kl.size() - 2];
+    }
+    if (!mode || Mpc != Mc || Krpc != 2 * Kc || Mc <= 128)
       throw Error(-1, "contract_planes: shapes do not allow plane output");
     const int64_t nsb = Kc / 128;
     auto digit = [&](char ch, int64_t& po, int64_t& so) {
@@ -593,8 +605,15 @@ static Tensor plane_output(Ctx& c, GemmDesc& g, const PlaneReq& rq, std::map<cha
     for (char ch : Ns) {
       int64_t po, so;
       digit(ch, po, so);
-      add(pout.vn, dim[ch], po, so);
+      if (mode == 2 && ch == outer) {  // split: (label / 4: block index, label % 4: inside a block)
+        const int64_t st = stride_in(kl, ch);  // = 32
+        add(pout.vn, dim[ch] / 4, 2 * st * 4, Mpc);
+        add(pout.vn, 4, 2 * st, 0);
+      } else {
+        add(pout.vn, dim[ch], po, so);
+      }
     }
+    pout.mode = mode;
     auto P = std::make_shared<Planes>();
     P->lab = zl + rl + kl;
     P->nz = (int)(c.nb * NZ);

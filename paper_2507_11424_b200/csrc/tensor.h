@@ -112,6 +112,7 @@ struct PlaneOut {
   float* asc = nullptr;
   PView vm, vn;
   int64_t zpo = 0, zso = 0;  // plane / scale stride of the GEMM's batch index (unfolded samples)
+  int mode = 1;              // scale block: 1 = a tile column of 128 rows, 2 = a warp's 32 rows x 4 columns
 };
 
 struct GemmDesc {

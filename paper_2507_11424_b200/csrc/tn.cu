@@ -305,7 +305,7 @@ int64_t per_sample_bytes(const Layout& L, int R, int chi) {
 // Whether a ladder GEMM (Y2 = Y1 . M_j or G2 = G1 . M_j) can write its closure's A planes
 // directly (contract_planes): rows = rbond x ebond (the closure's M, a whole number of CTA-pair
 // tiles), inner K = kbond = one scale block (128 complex), a down edge (d > 1), tensor-core GEMMs.
-// TN_LADDER_PLANES=0 disables it, =1 keeps only the G2 / Y2 planes (A/B measurements).
+// TN_LADDER_PLANES=0 disables it, =1 keeps only the G2 / Y2 planes, =2 adds G1 (A/B measurements).
 bool ladder_planes_ok(const Ctx& c, int rbond, int ebond, int d, int kbond) {
   static const bool off = getenv("TN_LADDER_PLANES") && std::atoi(getenv("TN_LADDER_PLANES")) == 0;
   if (off || c.gemm_mode == 1 || ebond <= 1 || d <= 1 || kbond != 128) return false;
@@ -313,6 +313,15 @@ bool ladder_planes_ok(const Ctx& c, int rbond, int ebond, int d, int kbond) {
   return rows % 256 == 0 && rows > 128 && ((int64_t)ebond * d) % 128 == 0 &&
          tc_eligible(c, (int64_t)rbond * 2 * kbond, (int64_t)ebond * d, (int64_t)d * ebond,
                      (int64_t)rbond * 2 * kbond * ebond * d * d * ebond);
+}
+
+// Whether Y1 = n_j . R (M = (a, s, d), N = (Z, f), K = z) can write Y2's A planes (rows (a, s, Z),
+// K = (f, d)): d = 32 is a warp's rows, 4 adjacent f complete a scale block (plane mode 2).
+bool y1_planes_ok(const Ctx& c, int a, int d, int f, int Z) {
+  static const bool off = getenv("TN_LADDER_PLANES") && std::atoi(getenv("TN_LADDER_PLANES")) < 3;
+  if (off || c.gemm_mode == 1 || d != 32 || f % 4 != 0 || a <= 1) return false;
+  const int64_t rows = (int64_t)a * 2 * Z;
+  return rows % 256 == 0 && ((int64_t)a * 2 * d) % 256 == 0 && ((int64_t)Z * f) % 128 == 0;
 }
 
 // Whether G1 = Lx . n_j[x] (M = (A, e), N = (d, z), K = a) can write G2's A planes (rows (z, A),
@@ -374,14 +383,24 @@ void sample_batch(tn_state* st, Layout& L, Envs& E, int R, int nb, const double*
     std::vector<Tensor> Rs(W);
     Tensor Rr = ones(c, {1, 1, 1}, nb);
     for (int j = W - 1; j >= 0; --j) {
-      Tensor Y1 = contract(c, n[j], "asdz", false, Rr, "zfZ", false, "asdfZ");
-      if (ladder_planes_ok(c, n[j].shape[0], ms.tops[j].p ? ms.tops[j].shape[0] : 0, n[j].shape[2], n[j].shape[3])) {
+      if (ladder_planes_ok(c, n[j].shape[0], ms.tops[j].p ? ms.tops[j].shape[0] : 0, n[j].shape[2], n[j].shape[3]) &&
+          y1_planes_ok(c, n[j].shape[0], n[j].shape[2], Rr.shape[1], Rr.shape[2])) {
+        // Y1 = n_j . R writes Y2's A planes (rows (a, s, Z), K = (f, d): blocks of a warp's 32 d
+        // x 4 f), Y2 = Y1 . M_j (planes in) writes the closure's (rows (a, e) per (sample, s),
+        // K = (D, Z)): the right pass has no complex64 ladder intermediate and no operand prep
+        Tensor Y1p = contract_planes(c, n[j], "asdz", false, Rr, "zfZ", false, "asdZf", "", "asZ", "fd");
+        Tensor Y2p = contract_planes(c, Y1p, "asZfd", false, ms.tops[j], "edDf", false, "asZeD", "s", "ae", "DZ");
+        Rs[j] = contract(c, Y2p, "saeDZ", false, n[j], "AsDZ", true, "saeA");
+      } else if (ladder_planes_ok(c, n[j].shape[0], ms.tops[j].p ? ms.tops[j].shape[0] : 0, n[j].shape[2],
+                                  n[j].shape[3])) {
         // Y2 = Y1 . M_j written by its GEMM straight into the FP16 A planes of the closure
         // Rs = Y2 . conj(n_j) (rows (a, e) per (sample, s), K = (D, Z)): no complex64 Y2 and no
         // operand prep for the closure
+        Tensor Y1 = contract(c, n[j], "asdz", false, Rr, "zfZ", false, "asdfZ");
         Tensor Y2p = contract_planes(c, Y1, "asdfZ", false, ms.tops[j], "edDf", false, "asZeD", "s", "ae", "DZ");
         Rs[j] = contract(c, Y2p, "saeDZ", false, n[j], "AsDZ", true, "saeA");
       } else {
+        Tensor Y1 = contract(c, n[j], "asdz", false, Rr, "zfZ", false, "asdfZ");
         Tensor Y2;
         if (ms.tops[j].p) Y2 = contract(c, Y1, "asdfZ", false, ms.tops[j], "edDf", false, "asZeD");
         else Y2 = permute(c, Y1, "asdfZ", "asZfd");  // identity: e = f, d = D = 1
