@@ -1,25 +1,27 @@
 // gemm_tc.cu -- complex GEMM on the 5th-generation tensor cores (tcgen05, sm_100a),
-// FP32-accurate through an FP16x3 split with exact power-of-two row/column scaling (K1 of
+// FP32-accurate through an FP16x3 split with exact power-of-two block scaling (K1 of
 // SURVEY 2.4).
 //
 // Complex C = A B is one real GEMM  C_r[M][2N] = A_r[M][2K] . B_r[2K][2N]:
 //   A_r = A viewed as interleaved (re, im) along K; C_r = C viewed the same way along N;
 //   B_r^T row 2n = (Re b_kn, -Im b_kn) over k, row 2n+1 = (Im b_kn, Re b_kn)  (K-major).
-// Each row m of A (each column n of B) is scaled by an exact power of two s so that its
-// largest |component| lies in [1/2, 1); every scaled value x is split into FP16 x = h + l
-// (h = fp16_rn(x), l = fp16_rn(x - h); 22 significant bits), and
-// D = A_h B_h + A_h B_l + A_l B_h accumulates in FP32; the epilogue multiplies by 1/(s_m s_n).
-// FP16 MMAs run at twice the TF32 rate and halve the operand bytes per K.
+// Every (row m of A, block of SB_K = 128 complex K) and (column n of B, block) is scaled by an
+// exact power of two s so that the block's largest |component| lies in [1/2, 1); every scaled
+// value x is split into FP16 x = h + l (h = fp16_rn(x), l = fp16_rn(x - h); 22 significant
+// bits), and D = A_h B_h + A_h B_l + A_l B_h accumulates in FP32 over one block in TMEM; the
+// epilogue promotes each block into FP32 registers multiplied by 1/(s_A s_B). FP16 MMAs run at
+// twice the TF32 rate and halve the operand bytes per K.
 //
-// Data flow: a max pass and a prep pass gather each operand straight from its multi-axis
-// layout (View4) into packed, zero-padded, K-major FP16 hi/lo planes in HBM; the GEMM kernel
-// streams 128x64 (A) and 256x64 (B) FP16 tiles with TMA (SWIZZLE_128B) through a 2-stage
-// mbarrier pipeline; one elected thread issues tcgen05.mma (M=128, N=256, K=16,
-// kind::f16, FP32 accumulate) into one of two 128x256 FP32 TMEM accumulators; every K chunk
-// of 1024 is promoted by eight epilogue warps into FP32 registers (the tensor core's FP32
-// accumulation truncates -- measured error grew linearly with K before chunking) while the
-// MMA fills the other accumulator. Long-K/small-MN GEMMs are split along K (deterministic
-// reduction).
+// Data flow: one prep pass gathers each operand straight from its multi-axis layout (View4)
+// into packed, zero-padded, K-major FP16 hi/lo planes in HBM, taking each block's scale from
+// the tile it converts -- or the producing GEMM's epilogue writes them (plane output, see
+// tc_gemm2_kernel<true>); the CTA-pair kernel streams FP16 tiles with TMA (SWIZZLE_128B)
+// through a 3-stage mbarrier ring; one elected thread issues tcgen05.mma (cta_group::2,
+// M=256, N=256, K=16, kind::f16, FP32 accumulate) into one of two TMEM accumulators; every
+// scale block is promoted by eight epilogue warps into FP32 registers (which also bounds the
+// tensor core's truncating FP32 accumulation) while the MMA fills the other accumulator.
+// Long-K/small-MN GEMMs are split along K (deterministic reduction). The 1-CTA kernel serves
+// GEMMs of <= 128 rows; the 3M kernel (off by default) keeps per-row scales.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
