@@ -100,7 +100,7 @@ __device__ __forceinline__ void pview_off(const PView& v, int64_t idx, int64_t& 
   po = 0;
   so = 0;
 #pragma unroll
-  for (int d = 3; d >= 0; --d) {
+  for (int d = 5; d >= 0; --d) {
     if (d < v.rank) {
       const int64_t q = idx / v.dims[d];
       const int64_t r = idx - q * v.dims[d];

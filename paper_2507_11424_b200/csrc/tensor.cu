@@ -557,7 +557,7 @@ static Tensor plane_output(Ctx& c, GemmDesc& g, const PlaneReq& rq, std::map<cha
     // digit, supplies 4 -- a block is a warp's 32 rows x 4 adjacent columns.
     int mode = 0;
     char outer = 0;
-    if (dim[inner] == 128 && Ms.back() == inner) mode = 1;
+    if (dim[inner] % 128 == 0 && Ms.back() == inner) mode = 1;
     else if (dim[inner] == 32 && Ms.back() == inner && kl.size() >= 2 && Ns.back() == kl[kl.size() - 2] &&
              dim[kl[kl.size() - 2]] % 4 == 0) {
       mode = 2;
@@ -586,7 +586,7 @@ static Tensor plane_output(Ctx& c, GemmDesc& g, const PlaneReq& rq, std::map<cha
     const bool folded = (g.M == Msz * c.nb) && c.nb > 1;
     if (!folded && g.M != Msz) throw Error(-1, "contract_planes: unexpected GEMM rows");
     auto add = [](PView& v, int d, int64_t po, int64_t so) {
-      if (v.rank >= 4) throw Error(-1, "contract_planes: more than four digits");
+      if (v.rank >= 6) throw Error(-1, "contract_planes: more than six digits");
       v.dims[v.rank] = d;
       v.po[v.rank] = po;
       v.so[v.rank] = so;
@@ -600,7 +600,12 @@ static Tensor plane_output(Ctx& c, GemmDesc& g, const PlaneReq& rq, std::map<cha
     for (char ch : Ms) {
       int64_t po, so;
       digit(ch, po, so);
-      add(pout.vm, dim[ch], po, so);
+      if (mode == 1 && ch == inner && dim[ch] > 128) {  // split: (label / 128: block, label % 128: a tile's rows)
+        add(pout.vm, dim[ch] / 128, 2 * 128, Mpc);
+        add(pout.vm, 128, 2, 0);
+      } else {
+        add(pout.vm, dim[ch], po, so);
+      }
     }
     for (char ch : Ns) {
       int64_t po, so;

@@ -99,12 +99,12 @@ struct View4 {
 // only): the operand preparation gathers straight from the multi-axis layout.
 // Plane output of a GEMM (contract_planes): element (m, n) of C goes to plane offset
 // po(m) + po(n) (halves) and its scale block to so(m) + so(n); each side decomposes its index
-// into up to four digits (outer -> inner) with a plane stride and a scale stride per digit.
+// into up to six digits (outer -> inner) with a plane stride and a scale stride per digit.
 struct PView {
   int rank = 0;
-  int dims[4] = {1, 1, 1, 1};
-  int64_t po[4] = {0, 0, 0, 0};
-  int64_t so[4] = {0, 0, 0, 0};
+  int dims[6] = {1, 1, 1, 1, 1, 1};
+  int64_t po[6] = {0, 0, 0, 0, 0, 0};
+  int64_t so[6] = {0, 0, 0, 0, 0, 0};
 };
 struct PlaneOut {
   __half* hi = nullptr;

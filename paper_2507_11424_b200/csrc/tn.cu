@@ -304,11 +304,12 @@ int64_t per_sample_bytes(const Layout& L, int R, int chi) {
 // are (near) exact): the n-fits' log-norms, the merge normalisations and the final scalar.
 // Whether a ladder GEMM (Y2 = Y1 . M_j or G2 = G1 . M_j) can write its closure's A planes
 // directly (contract_planes): rows = rbond x ebond (the closure's M, a whole number of CTA-pair
-// tiles), inner K = kbond = one scale block (128 complex), a down edge (d > 1), tensor-core GEMMs.
+// tiles), inner K = kbond = whole scale blocks (multiples of 128 complex: a CTA tile's 128 rows
+// are one block), a down edge (d > 1), tensor-core GEMMs.
 // TN_LADDER_PLANES=0 disables it, =1 keeps only the G2 / Y2 planes, =2 adds G1 (A/B measurements).
 bool ladder_planes_ok(const Ctx& c, int rbond, int ebond, int d, int kbond) {
   static const bool off = getenv("TN_LADDER_PLANES") && std::atoi(getenv("TN_LADDER_PLANES")) == 0;
-  if (off || c.gemm_mode == 1 || ebond <= 1 || d <= 1 || kbond != 128) return false;
+  if (off || c.gemm_mode == 1 || ebond <= 1 || d <= 1 || kbond % 128 != 0) return false;
   const int64_t rows = (int64_t)rbond * ebond;
   return rows % 256 == 0 && rows > 128 && ((int64_t)ebond * d) % 128 == 0 &&
          tc_eligible(c, (int64_t)rbond * 2 * kbond, (int64_t)ebond * d, (int64_t)d * ebond,
@@ -325,10 +326,10 @@ bool y1_planes_ok(const Ctx& c, int a, int d, int f, int Z) {
 }
 
 // Whether G1 = Lx . n_j[x] (M = (A, e), N = (d, z), K = a) can write G2's A planes (rows (z, A),
-// K = (d, e)): e is one scale block, whole CTA-pair tiles, a down edge.
+// K = (d, e)): e is whole scale blocks, whole CTA-pair tiles, a down edge.
 bool g1_planes_ok(const Ctx& c, int e, int A, int d, int z) {
   static const bool off = getenv("TN_LADDER_PLANES") && std::atoi(getenv("TN_LADDER_PLANES")) < 2;
-  if (off || c.gemm_mode == 1 || e != 128 || d <= 1 || A <= 1) return false;
+  if (off || c.gemm_mode == 1 || e % 128 != 0 || d <= 1 || A <= 1) return false;
   const int64_t rows = (int64_t)z * A;
   return rows % 256 == 0 && ((int64_t)A * e) % 256 == 0 && ((int64_t)d * z) % 128 == 0;
 }

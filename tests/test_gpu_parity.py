@@ -159,6 +159,30 @@ def test_branch_superposition_metric_shapes_exact():
         assert abs(logq[k] - sum(math.log(r) for r in ref)) <= 1e-4 * max(1, abs(logq[k]))
 
 
+def test_branch_superposition_env256_plane_blocks_exact():
+    """chi_env = 256 on three full-width Willow rows (chi = 32, K = 11 branches: exact, as in
+    the metric-shape test): the ladder GEMMs' plane outputs then carry two scale blocks per inner
+    K digit (the digit of 256 split into block x 128 rows of a CTA tile); every conditional and
+    ln q against the closed form, and the plane path must have run."""
+    import ctypes
+    from paper_2507_11424_b200 import _lib
+    from tests.test_oracle import closed_form_conditionals
+    lat = L.row_strip(L.willow105(), 1, 4)
+    st = S.branch_superposition(lat, 32, 11, seed=23)
+    u = S.uniforms(2, lat.n, 41)
+    _lib.lib().tn_debug_plane_gemms.restype = ctypes.c_int64
+    _lib.lib().tn_debug_plane_gemms(1)
+    g, bits, logq, cond, flags = _run(st, lat.rows, 256, u)
+    assert _lib.lib().tn_debug_plane_gemms(1) > 0
+    order = order_of(lat.rows)
+    assert (flags == 0).all()
+    for k in range(len(u)):
+        ref = closed_form_conditionals(st["meta"]["phis"], order, bits[k])
+        for v, r in zip(order, ref):
+            assert abs(cond[k, v] - r) <= 1e-4 * r + (1e-6 if r < 1e-2 else 0), (k, v, cond[k, v], r)
+        assert abs(logq[k] - sum(math.log(r) for r in ref)) <= 1e-4 * max(1, abs(logq[k]))
+
+
 def test_metric_shapes_batch_composition_bitwise():
     """The metric-shape ladder runs through the plane-output GEMMs (the ladder GEMMs write their
     closures' FP16 A planes and block scales from the epilogue; G1 -> G2 -> Lx chained, the
